@@ -1,0 +1,168 @@
+// synth/synth_gpu.cu -- point-scatterer channel-data generator on the GPU.
+//
+// INPUT GENERATION ONLY (harness; SPEC synth module S:410-460).  Same
+// forward model as synth.c (see its header) in float32, used to produce the
+// large C2/C3/C4 frames in seconds on the box.  No method arithmetic lives
+// here.  Deterministic: per-trace sums are accumulated in shared memory as
+// 32-bit fixed point with integer atomics (associative), scaled by a bound
+// computed in a first pass, so every run writes the same int16 buffer.
+//
+// Passes per frame:
+//   0  bound   B = max_trace sum_s |a_s| / (d_tx d_rx)        (fixed-point scale 2^30/B)
+//   1  peak    P = max |sum| over the frame (noiseless)
+//   2  write   out = rint(sum * (32767/4)/P + noise)           (12 dB headroom)
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace {
+
+struct SynP {
+  int nx, ny;
+  float px, py;
+  int E, S;
+  float smm;     // fs / (1000 c): samples per mm of path
+  float sigma;   // pulse sigma in samples
+  float w0;      // 2 pi f0 / fs
+};
+
+__device__ __forceinline__ void elem_pos(const SynP& p, int ch, float& ex, float& ey) {
+  int i = ch % p.nx, j = ch / p.nx;
+  ex = (i - (p.nx - 1) * 0.5f) * p.px;
+  ey = (j - (p.ny - 1) * 0.5f) * p.py;
+}
+
+__global__ void k_bound(SynP p, const float4* __restrict__ scat, int n,
+                        const float* __restrict__ tx, unsigned* __restrict__ bound_bits) {
+  const int C = p.nx * p.ny;
+  const int tr = blockIdx.x;
+  const int ev = tr / C, ch = tr % C;
+  float ex, ey;
+  elem_pos(p, ch, ex, ey);
+  const float tx0 = tx[3 * ev], tx1 = tx[3 * ev + 1], tx2 = tx[3 * ev + 2];
+  float acc = 0.f;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+    float4 q = scat[s];
+    float dtx = sqrtf((q.x - tx0) * (q.x - tx0) + (q.y - tx1) * (q.y - tx1) + (q.z - tx2) * (q.z - tx2));
+    float drx = sqrtf((q.x - ex) * (q.x - ex) + (q.y - ey) * (q.y - ey) + q.z * q.z);
+    if (dtx > 0.f && drx > 0.f) acc += fabsf(q.w) / (dtx * drx);
+  }
+  __shared__ float red[1024];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(bound_bits, __float_as_uint(red[0]));
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ float gauss(uint64_t seed, uint64_t idx) {
+  uint64_t h1 = mix64((seed << 40) ^ (2 * idx));
+  uint64_t h2 = mix64((seed << 40) ^ (2 * idx + 1));
+  double u1 = ((h1 >> 11) + 1) * (1.0 / 9007199254740992.0);
+  double u2 = (h2 >> 11) * (1.0 / 9007199254740992.0);
+  return (float)(sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+}
+
+// mode 1: peak pass (atomicMax of |sum|);  mode 2: write int16.
+template <int MODE>
+__global__ void k_trace(SynP p, const float4* __restrict__ scat, int n, const float* __restrict__ tx,
+                        const unsigned* __restrict__ bound_bits, int* __restrict__ peak_fixed,
+                        int16_t* __restrict__ out, unsigned long long seed, float noise_rel) {
+  extern __shared__ int trace[];
+  const int C = p.nx * p.ny;
+  const int tr = blockIdx.x;
+  const int ev = tr / C, ch = tr % C;
+  const int S = p.S;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) trace[i] = 0;
+  __syncthreads();
+  const float B = __uint_as_float(*bound_bits);
+  const float fx = (B > 0.f) ? 1073741824.f / B : 0.f;
+  float ex, ey;
+  elem_pos(p, ch, ex, ey);
+  const float tx0 = tx[3 * ev], tx1 = tx[3 * ev + 1], tx2 = tx[3 * ev + 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const float half = 4.f * p.sigma, inv2s2 = 1.f / (2.f * p.sigma * p.sigma);
+  for (int s = warp; s < n; s += nw) {
+    float4 q = scat[s];
+    float dtx = sqrtf((q.x - tx0) * (q.x - tx0) + (q.y - tx1) * (q.y - tx1) + (q.z - tx2) * (q.z - tx2));
+    float drx = sqrtf((q.x - ex) * (q.x - ex) + (q.y - ey) * (q.y - ey) + q.z * q.z);
+    if (!(dtx > 0.f && drx > 0.f)) continue;
+    float arr = (dtx + drx) * p.smm;
+    float amp = q.w / (dtx * drx) * fx;
+    int lo = (int)ceilf(arr - half), hi = (int)floorf(arr + half);
+    lo = max(lo, 0);
+    hi = min(hi, S - 1);
+    for (int i = lo + lane; i <= hi; i += 32) {
+      float t = i - arr;
+      float g = __expf(-t * t * inv2s2) * __cosf(p.w0 * t);
+      atomicAdd(&trace[i], __float2int_rn(amp * g));
+    }
+  }
+  __syncthreads();
+  if (MODE == 1) {
+    int m = 0;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) m = max(m, abs(trace[i]));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) atomicMax(peak_fixed, m);
+  } else {
+    const int P = *peak_fixed;
+    const float scale = (P > 0) ? 8191.75f / (float)P : 0.f;
+    const float nz = noise_rel * 8191.75f;  // noise std in output units (re the peak)
+    int16_t* o = out + (size_t)tr * S;
+    const uint64_t base = (uint64_t)tr * (uint64_t)S;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+      float x = (float)trace[i] * scale;
+      if (noise_rel > 0.f) x += nz * gauss(seed, base + i);
+      float v = rintf(x);
+      v = fminf(fmaxf(v, -32768.f), 32767.f);
+      o[i] = (int16_t)v;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// Generate one frame [E][C][S] int16 on the device.
+//   scat_dev: [n] float4 (x, y, z, reflectivity) mm;  tx_dev: [E][3] float mm;
+//   scratch_dev: >= 2 uint32 (zeroed here);  noise_rel <= 0 disables noise.
+// Returns 0 or a cudaError_t value.
+int syn_gpu_frame(int nx, int ny, double px, double py, int E, int S, double fs_hz, double c_mps,
+                  double f0_hz, double fbw, const void* scat_dev, int n, const void* tx_dev,
+                  void* out_dev, void* scratch_dev, unsigned long long seed, double noise_rel,
+                  void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  SynP p;
+  p.nx = nx; p.ny = ny; p.px = (float)px; p.py = (float)py; p.E = E; p.S = S;
+  p.smm = (float)(fs_hz / (1000.0 * c_mps));
+  double sigma_f = fbw * f0_hz / (2.0 * 1.1774100225154747);
+  p.sigma = (float)(fs_hz / (6.283185307179586 * sigma_f));
+  p.w0 = (float)(6.283185307179586 * f0_hz / fs_hz);
+  unsigned* bound = (unsigned*)scratch_dev;
+  int* peak = (int*)scratch_dev + 1;
+  cudaMemsetAsync(scratch_dev, 0, 8, st);
+  const int traces = E * nx * ny;
+  if (traces == 0) return 0;
+  k_bound<<<traces, 256, 0, st>>>(p, (const float4*)scat_dev, n, (const float*)tx_dev, bound);
+  size_t sm = (size_t)S * sizeof(int);
+  if (sm > 48 * 1024) {
+    cudaFuncSetAttribute(k_trace<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_trace<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  }
+  k_trace<1><<<traces, 256, sm, st>>>(p, (const float4*)scat_dev, n, (const float*)tx_dev, bound,
+                                      peak, nullptr, seed, (float)noise_rel);
+  k_trace<2><<<traces, 256, sm, st>>>(p, (const float4*)scat_dev, n, (const float*)tx_dev, bound,
+                                      peak, (int16_t*)out_dev, seed, (float)noise_rel);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"
