@@ -1,0 +1,215 @@
+/*
+ * supra_bf.h -- C ABI of the B200-native SUPRA receive-beamforming hot path.
+ *
+ * The library implements the data-parallel steps of the software ultrasound
+ * pipeline of Goebl, Navab, Hennersperger, "SUPRA: Open Source Software
+ * Defined Ultrasound Processing for Real-Time Applications" (arXiv
+ * 1711.06127), section 2 (P:95-100, P:117-123 of /root/reference/PAPER.md):
+ *
+ *   raw channel data --(delay-and-sum receive beamforming)--> RF
+ *                    --(IQ envelope + log compression, fused)--> line image
+ *                    --(scan conversion, separate kernel)--> B-mode image
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n (interfaces and
+ * defaults only); "reading #n" = DESIGN.md "Readings",
+ * where the paper is silent.  Units: mm, Hz, m/s, s, degrees.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  * All data buffers are CALLER-OWNED device memory on cfg.device,
+ *    contiguous, in the layouts stated below.  The library never frees or
+ *    retains them beyond the call and never allocates per call, so every call
+ *    is capturable in a CUDA graph.
+ *  * Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL
+ *    = legacy default stream).  Validation errors are returned synchronously
+ *    before anything is enqueued.  A device fault raised by an earlier launch
+ *    surfaces as SUPRA_E_CUDA on a later call.
+ *  * A handle owns its device tables and per-frame scratch; it must not be
+ *    used concurrently from two streams (create one handle per stream/GPU).
+ *    Two handles may read the same raw buffer (the paper's "two differently
+ *    parametrized beamforming runs in parallel on the same input").
+ *  * There is no CPU fallback: without a usable CUDA device `supra_bf_create`
+ *    returns SUPRA_E_CUDA.
+ */
+#ifndef SUPRA_BF_H
+#define SUPRA_BF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SUPRA_BF_ABI_VERSION 1
+
+typedef struct supra_bf *supra_bf_t;
+
+typedef enum {
+    SUPRA_OK = 0,
+    SUPRA_E_PARAM = 2,    /* a parameter outside its declared range */
+    SUPRA_E_STRUCT = 3,   /* NULL / shape / alignment / device mismatch, line_event out of range */
+    SUPRA_E_RESOURCE = 4, /* device memory for tables or scratch could not be allocated */
+    SUPRA_E_CUDA = 5      /* CUDA runtime / launch error, or no usable device */
+} supra_status;
+
+enum { SUPRA_WIN_RECT = 0, SUPRA_WIN_HANN = 1, SUPRA_WIN_HAMMING = 2 }; /* receive window */
+enum { SUPRA_NORM_COUNT = 0, SUPRA_NORM_NONE = 1 };   /* sum / #members (reading #7) or plain sum */
+enum { SUPRA_REF_FRAME_MAX = 0, SUPRA_REF_FIXED = 1 };/* log reference */
+enum { SUPRA_T_I16 = 0, SUPRA_T_F32 = 1, SUPRA_T_U8 = 2 };
+enum { SUPRA_SC_LINEAR_2D = 0, SUPRA_SC_SECTOR_2D = 1, SUPRA_SC_PYRAMID_3D = 2 };
+
+/*
+ * Configuration.  `supra_bf_create` copies every field and array; the caller
+ * may free them afterwards.  Ranges checked at create (else SUPRA_E_PARAM):
+ *   elements_x, elements_y >= 1, pitch > 0, center_frequency > 0;
+ *   num_events >= 1; samples_per_channel >= 16 and a multiple of 8 (16-byte
+ *   rows for the bulk-copy staging); input_type = SUPRA_T_I16;
+ *   sample_frequency > 0; speed_of_sound in [1000, 2000];
+ *   f_number > 0; window, normalize in their enums;
+ *   fir_taps odd, 1..129; decimation = 1 (>1 is future work);
+ *   0 < demod_frequency - bw/2 and demod_frequency + bw/2 < fs/2 (S:188,
+ *   S:196); dynamic_range_db > 0; reference_value > 0 when
+ *   reference_mode = FIXED; spacing > 0 and out_dims >= 1;
+ *   0 < fov < 180 degrees for SECTOR / PYRAMID;
+ *   max_frames_per_call >= 1.
+ * Scanline geometry must match sc_kind (else SUPRA_E_PARAM), because scan
+ * conversion inverts it analytically (reading #13/#14):
+ *   LINEAR_2D : num_lines_y = 1, num_lines_x >= 2, directions (0,0,1),
+ *               origins (x_l, 0, 0) evenly spaced and increasing (1e-9 rel);
+ *   SECTOR_2D : num_lines_y = 1, num_lines_x >= 2, origins 0, directions
+ *               (sin t_l, 0, cos t_l), t_l = (l - (L-1)/2) fov_x/(L-1) (1e-9);
+ *   PYRAMID_3D: num_lines_x, num_lines_y >= 2, origins 0, line l = ly*Lx + lx
+ *               with direction (sin tx, cos tx sin ty, cos tx cos ty).
+ * line_event[l] in [0, num_events) else SUPRA_E_STRUCT.
+ */
+typedef struct {
+    int32_t abi_version;          /* SUPRA_BF_ABI_VERSION */
+    int32_t device;               /* CUDA ordinal; every buffer must live on it */
+    /* transducer: element (i,j) at ((i-(Nx-1)/2) px, (j-(Ny-1)/2) py, 0), channel j*Nx+i */
+    int32_t elements_x, elements_y;
+    double pitch_x_mm, pitch_y_mm;
+    double center_frequency_hz;
+    /* acquisition: raw frame [num_events][channels][samples], time fastest */
+    int32_t num_events, samples_per_channel;
+    int32_t input_type;           /* SUPRA_T_I16 */
+    double sample_frequency_hz, speed_of_sound_mps;
+    double t0_s;                  /* time of sample 0 after the transmit (reading #3); 0 = default */
+    /* scanlines ("fully flexible scanline layout") */
+    int32_t num_lines_x, num_lines_y;  /* L = Lx*Ly, l = ly*Lx + lx */
+    const double *line_origin_mm;      /* [L][3], on the array face (z = 0) */
+    const double *line_direction;      /* [L][3], unit within 1e-9 */
+    const int32_t *line_event;         /* [L], multi-line map */
+    /* receive beamforming */
+    double f_number;
+    int32_t window, normalize;
+    /* envelope: demodulation at f_d, low-pass cutoff bw/2 */
+    double demod_frequency_hz, demod_bandwidth_hz;
+    int32_t fir_taps, decimation;
+    /* log compression */
+    double dynamic_range_db, reference_value;
+    int32_t reference_mode, line_output_type;  /* line image: SUPRA_T_F32 (y in [0,1]) or SUPRA_T_U8 */
+    /* scan conversion */
+    int32_t sc_kind, sc_output_type;           /* output: SUPRA_T_F32 or SUPRA_T_U8 */
+    int32_t out_dims[3];                       /* nx, ny, nz (ny = 1 for 2D) */
+    double out_origin_mm[3], out_spacing_mm[3];/* pixel (ix,iy,iz) at origin + i*spacing */
+    double fov_x_deg, fov_y_deg;
+    int32_t max_frames_per_call;               /* sizes the per-frame scratch */
+} supra_bf_config;
+
+/*
+ * supra_bf_create -- validate `cfg`, build the per-configuration tables in
+ * binary64 on the host, and upload them (the only host->device traffic the
+ * library itself causes).  Tables: per-line aperture entries sorted by
+ * aperture entry depth k_enter = min{k : (2F) rho <= k dr} (reading
+ * #6), element offsets in sample units, complex FIR taps, and the
+ * scan-conversion index/fraction table (reading #21/#22).
+ *   cfg : host pointer, read only during the call.
+ *   out : receives the handle on SUPRA_OK, NULL otherwise.
+ * Errors: SUPRA_E_PARAM / SUPRA_E_STRUCT (see the config comment),
+ * SUPRA_E_RESOURCE (cudaMalloc), SUPRA_E_CUDA (no device / runtime error).
+ */
+supra_status supra_bf_create(const supra_bf_config *cfg, supra_bf_t *out);
+
+/*
+ * supra_bf_beamform -- delay-and-sum receive beamforming with dynamic receive
+ * focusing, optionally followed by the
+ * fused IQ envelope and log compression (P:69,
+ * P:122).  For line l, output sample k, z = k dr, dr = c/(2 fs):
+ *   RF[l][k] = sum_{e : (2F) rho_le <= z} w(rho_le/R) x~_{ev(l),e}(tau_le(k)) / N
+ *   tau = (z + |o_l + z d_l - pos_e|) fs/c + t0 fs, linear interpolation,
+ *   zero outside [0, S) (reading #10), R = z/(2F), N = #members (0 -> 0).
+ *   env[k] = 2 |sum_{j=-P..P} h_j RF[k-j] e^{-i w (k-j)}|  (w = 2 pi f_d / fs)
+ *   y = 0 if env = 0, else clamp((20 log10(env/ref) + DR)/DR, 0, 1),
+ *   ref = per-frame max of env (SUPRA_REF_FRAME_MAX) or reference_value.
+ * Arguments:
+ *   raw      : device, int16 [frames][num_events][channels][samples], 16-byte aligned.
+ *   frames   : 0 .. max_frames_per_call (0 = no-op).
+ *   rf       : device float [frames][L][samples] or NULL.
+ *   line_img : device [frames][L][samples] of line_output_type or NULL
+ *              (non-NULL runs the fused envelope + log epilogue).
+ *   stream   : cudaStream_t.
+ * Errors: SUPRA_E_STRUCT if both outputs are NULL, raw is NULL/misaligned,
+ * frames out of range, or a pointer is not device memory of cfg.device.
+ */
+supra_status supra_bf_beamform(supra_bf_t h, const void *raw, int32_t frames, float *rf,
+                               void *line_img, void *stream);
+
+/*
+ * supra_bf_envelope_log -- the unfused epilogue on an RF buffer: IQ envelope
+ * + log compression exactly as above, for `frames` frames.
+ *   rf       : device float [frames][L][samples].
+ *   line_img : device [frames][L][samples] of line_output_type.
+ * Errors: SUPRA_E_STRUCT on NULL / frames out of range.
+ */
+supra_status supra_bf_envelope_log(supra_bf_t h, const float *rf, int32_t frames, void *line_img,
+                                   void *stream);
+
+/*
+ * supra_bf_scanconvert -- scan conversion in 2D and 3D (S:285-
+ * 311): per output pixel/voxel the create-time table gives validity, integer
+ * indices (built in binary64, bit-exact with the analytic inverse map) and
+ * fractions; the log-compressed line image is blended bilinearly (2D) or
+ * trilinearly (3D) (reading #23).  Invalid pixels are 0 with mask 0.
+ *   line_img : device [frames][Ly][Lx][samples] of line_output_type.
+ *   img      : device [frames][nz][ny][nx] of sc_output_type (x fastest).
+ *   mask     : device uint8 [nz][ny][nx] or NULL (frame-independent).
+ * Errors: SUPRA_E_STRUCT on NULL / frames out of range.
+ */
+supra_status supra_bf_scanconvert(supra_bf_t h, const void *line_img, int32_t frames, void *img,
+                                  uint8_t *mask, void *stream);
+
+/*
+ * supra_bf_destroy -- synchronise the device and free the handle's tables and
+ * scratch.  NULL is a no-op.
+ */
+void supra_bf_destroy(supra_bf_t h);
+
+/* ---- introspection (tests, bench) ------------------------------------ */
+
+/* Human-readable text of the last error on this thread ("" if none). */
+const char *supra_bf_last_error(void);
+
+/*
+ * supra_bf_sc_indices -- copy the scan-conversion table's integer part to
+ * host memory for bit-exact comparison with an independent inverse map:
+ * for every output pixel n (x fastest): valid[n] in {0,1} and
+ * idx[3n..3n+2] = (i0x, i0y, k0) as int32 (undefined where valid = 0).
+ *   valid : host uint8 [nz*ny*nx];  idx : host int32 [nz*ny*nx][3].
+ * Synchronous.  Errors: SUPRA_E_STRUCT on NULL.
+ */
+supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t *valid, int32_t *idx);
+
+/*
+ * supra_bf_info -- launch facts for the bench (host int64 [8]):
+ *   [0] kernels launched per beamform call with line_img (DAS + finalize),
+ *   [1] DAS frames batched per CTA, [2] DAS depth tile, [3] referenced input
+ *   bytes per frame (distinct int16 samples any tap reads x 2),
+ *   [4] taps per frame, [5] scan-conversion table bytes, [6] valid output
+ *   pixels, [7] kernels per scanconvert call.
+ */
+supra_status supra_bf_info(supra_bf_t h, int64_t *info8);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUPRA_BF_H */

@@ -1,0 +1,64 @@
+"""Build libsupra_bf.so in-tree: sm_100a kernels (nvcc) + binary64 host library
+(g++ -ffp-contract=off).  ``python -m paper_1711_06127_b200.build``."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libsupra_bf.so")
+BUILD = os.path.join(HERE, "_build")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU = ["das.cu", "epilogue.cu", "scanconv.cu"]
+CPP = ["host.cpp"]
+HDRS = ["internal.h", "epilogue.cuh"]
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+
+
+def _stale(out, deps):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    hdr_deps = [os.path.join(CSRC, h) for h in HDRS] + [os.path.join(ROOT, "include", "supra_bf.h")]
+    objs = []
+    for f in CU:
+        src = os.path.join(CSRC, f)
+        obj = os.path.join(BUILD, f + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + hdr_deps):
+            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
+                   "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", *inc, "-c", src, "-o", obj]
+            if ptxas_v:
+                cmd.insert(1, "-Xptxas=-v")
+            _run(cmd, verbose)
+    for f in CPP:
+        src = os.path.join(CSRC, f)
+        obj = os.path.join(BUILD, f + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + hdr_deps):
+            _run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                  "-Wall", "-I", os.path.join(CUDA, "include"), *inc, "-c", src, "-o", obj], verbose)
+    if force or _stale(OUT, objs):
+        _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-o", OUT, *objs,
+              "-Xcompiler", "-fPIC", "-cudart", "static"], verbose)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv)
+    print(OUT)

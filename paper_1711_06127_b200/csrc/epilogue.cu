@@ -1,0 +1,97 @@
+// epilogue.cu -- standalone IQ envelope + log compression on an RF buffer
+// (supra_bf_envelope_log) and the frame-max finalisation shared with the
+// fused path.
+#include "epilogue.cuh"
+
+namespace supra {
+
+// One CTA per (line, frame): the RF line is staged in shared memory with
+// zeroed FIR halos, then the same epilogue as the fused DAS path runs.
+__global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int S = a.S, T = a.fir_taps, P = (T - 1) / 2;
+  float2* fir = (float2*)smem_raw;
+  float* rfs = (float*)(smem_raw + ((sizeof(float2) * T + 15) & ~size_t(15)));
+  unsigned* smax = (unsigned*)(rfs + S + 2 * P);
+  const int line = blockIdx.x, f = blockIdx.y;
+  const float* src = a.rf + ((size_t)f * a.L + line) * S;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) fir[i] = a.fir[i];
+  for (int i = threadIdx.x; i < S + 2 * P; i += blockDim.x) {
+    int k = i - P;
+    rfs[i] = (k >= 0 && k < S) ? src[k] : 0.f;
+  }
+  if (threadIdx.x < 8) smax[threadIdx.x] = 0u;
+  __syncthreads();
+  fused_epilogue<1>(rfs, fir, T, S, a.L, line, f, a.F, a.ref_fixed, a.log_k1, a.log_k0, a.env_out,
+                    a.y_out, a.y_type, a.frame_max, smax);
+}
+
+// y = 1 + (20 log10 2 / DR) (log2 env - log2 ref), clamped to [0,1]; env = 0
+// or an all-zero frame -> 0.  Grid-stride, 4 samples/thread.
+__global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
+  const long long per = a.per_frame;
+  const long long total = per * a.F;
+  const long long n4 = total >> 2;
+  const bool vec = (per & 3) == 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (vec ? n4 : total); i += stride) {
+    const long long e0 = vec ? i * 4 : i;
+    const int f = (int)(e0 / per);
+    const float ref = __uint_as_float(a.frame_max[f]);
+    const float lref = ref > 0.f ? log2f(ref) : 0.f;
+    float v[4];
+    int n = vec ? 4 : 1;
+    if (vec) {
+      float4 x = reinterpret_cast<const float4*>(a.env)[i];
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+      v[0] = a.env[e0];
+    }
+    float y[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j < n) {
+        float e = v[j];
+        y[j] = (e > 0.f && ref > 0.f) ? fminf(fmaxf(fmaf(a.DR_k, log2f(e) - lref, 1.f), 0.f), 1.f) : 0.f;
+      }
+    }
+    if (a.y_type == SUPRA_T_U8) {
+      uint8_t* o = (uint8_t*)a.y_out;
+      if (vec) {
+        uchar4 q;
+        q.x = (uint8_t)floorf(255.f * y[0] + 0.5f);
+        q.y = (uint8_t)floorf(255.f * y[1] + 0.5f);
+        q.z = (uint8_t)floorf(255.f * y[2] + 0.5f);
+        q.w = (uint8_t)floorf(255.f * y[3] + 0.5f);
+        reinterpret_cast<uchar4*>(o)[i] = q;
+      } else {
+        o[e0] = (uint8_t)floorf(255.f * y[0] + 0.5f);
+      }
+    } else {
+      float* o = (float*)a.y_out;
+      if (vec) reinterpret_cast<float4*>(o)[i] = make_float4(y[0], y[1], y[2], y[3]);
+      else o[e0] = y[0];
+    }
+  }
+}
+
+cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st) {
+  const int P = (a.fir_taps - 1) / 2;
+  size_t smem = ((sizeof(float2) * a.fir_taps + 15) & ~size_t(15)) + sizeof(float) * (a.S + 2 * P) + 64;
+  cudaError_t e = cudaFuncSetAttribute(envlog_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(a.L, a.F);
+  envlog_kernel<<<grid, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
+  long long total = a.per_frame * a.F;
+  long long work = (a.per_frame & 3) == 0 ? total / 4 : total;
+  int blocks = (int)std::min<long long>((work + 255) / 256, 148LL * 16);
+  if (blocks < 1) blocks = 1;
+  finalize_kernel<<<blocks, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace supra

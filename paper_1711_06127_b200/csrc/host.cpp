@@ -1,0 +1,741 @@
+// host.cpp -- C-ABI host library: validation, binary64 setup tables, launches.
+//
+// Implements include/supra_bf.h.  Table construction runs once per
+// configuration on the host in IEEE binary64 (compiled -ffp-contract=off) so
+// every discontinuous decision -- aperture membership and scan-conversion
+// indices -- is taken with the canonical expressions stated in DESIGN.md
+// "Readings" (#6, #21, #22) and is bit-exact with any other binary64
+// evaluation of the same definition.  Per-frame work runs in the sm_100a
+// kernels (das.cu, epilogue.cu, scanconv.cu); there is no CPU fallback.
+#include "supra_bf.h"
+#include "internal.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+using namespace supra;
+
+namespace {
+
+thread_local std::string g_err;
+
+supra_status fail(supra_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+supra_status fail(supra_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+constexpr double kPi = 3.14159265358979323846;
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct supra_bf {
+  supra_bf_config cfg{};
+  int L = 0, C = 0, S = 0, E = 0, G = 0;
+  int ntiles = 0, entries_per_group = 0;
+  int frames_per_cta = 1;
+  size_t das_smem = 0;
+  double dr_mm = 0.0, s_per_mm = 0.0;
+  // device tables
+  int32_t* d_line_group = nullptr;
+  DasEntry* d_entries = nullptr;
+  int32_t* d_ntile = nullptr;
+  float4* d_line_dir = nullptr;
+  int32_t* d_line_event = nullptr;
+  float2* d_fir = nullptr;
+  unsigned* d_frame_max = nullptr;
+  float* d_env = nullptr;
+  ScAxis* d_ax = nullptr;
+  ScAxis* d_az = nullptr;
+  ScRow* d_rows = nullptr;
+  ScEntry* d_ent = nullptr;
+  // host copies for introspection
+  std::vector<ScAxis> h_ax, h_az;
+  std::vector<ScRow> h_rows;
+  std::vector<ScEntry> h_ent;
+  int64_t info[8] = {0};
+};
+
+namespace {
+
+template <class T>
+cudaError_t upload(T** d, const std::vector<T>& h) {
+  *d = nullptr;
+  if (h.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void**)d, h.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+void free_all(supra_bf* h) {
+  void* ptrs[] = {h->d_line_group, h->d_entries, h->d_ntile, h->d_line_dir, h->d_line_event,
+                  h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_rows, h->d_ent};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+// Element (i,j) position, S:30 (same definition the oracle writes out).
+inline void elem_pos(const supra_bf_config& c, int ch, double* p) {
+  int i = ch % c.elements_x, j = ch / c.elements_x;
+  p[0] = (i - (c.elements_x - 1) / 2.0) * c.pitch_x_mm;
+  p[1] = (j - (c.elements_y - 1) / 2.0) * c.pitch_y_mm;
+  p[2] = 0.0;
+}
+
+// Canonical aperture predicate (reading #6): (2F) rho <= k dr, binary64.
+inline bool member(double F, double rho, int k, double dr) { return (2.0 * F) * rho <= k * dr; }
+
+int k_enter(double F, double rho, double dr, int S) {
+  double g = std::ceil((2.0 * F) * rho / dr);
+  long k = (g < 0) ? 0 : (g > S + 2.0 ? (long)S + 2 : (long)g);
+  while (k > 0 && member(F, rho, (int)k - 1, dr)) k--;
+  while (k <= S && !member(F, rho, (int)k, dr)) k++;
+  return (int)std::min<long>(k, S);
+}
+
+// tau in samples for element e, line (o,d), output sample k (binary64).
+double tau_d(const double* o, const double* d, const double* e, int k, double dr, double fs,
+             double c, double t0) {
+  double z = k * dr;
+  double p0 = o[0] + z * d[0] - e[0], p1 = o[1] + z * d[1] - e[1], p2 = o[2] + z * d[2] - e[2];
+  double r = std::sqrt(p0 * p0 + p1 * p1 + p2 * p2);
+  return ((z + r) / 1000.0) * fs / c + t0 * fs;
+}
+
+supra_status validate(const supra_bf_config* c) {
+  if (!c) return fail(SUPRA_E_STRUCT, "cfg is NULL");
+  if (c->abi_version != SUPRA_BF_ABI_VERSION)
+    return fail(SUPRA_E_PARAM, "abi_version %d != %d", c->abi_version, SUPRA_BF_ABI_VERSION);
+  if (c->elements_x < 1 || c->elements_y < 1) return fail(SUPRA_E_PARAM, "elements must be >= 1");
+  if (!(c->pitch_x_mm > 0) || !(c->pitch_y_mm > 0)) return fail(SUPRA_E_PARAM, "pitch must be > 0");
+  if (!(c->center_frequency_hz > 0)) return fail(SUPRA_E_PARAM, "center_frequency must be > 0");
+  if (c->num_events < 1) return fail(SUPRA_E_PARAM, "num_events must be >= 1");
+  if (c->samples_per_channel < 16 || c->samples_per_channel % 8 != 0)
+    return fail(SUPRA_E_PARAM, "samples_per_channel must be >= 16 and a multiple of 8");
+  if (c->input_type != SUPRA_T_I16) return fail(SUPRA_E_PARAM, "input_type must be SUPRA_T_I16");
+  if (!(c->sample_frequency_hz > 0)) return fail(SUPRA_E_PARAM, "sample_frequency must be > 0");
+  if (!(c->speed_of_sound_mps >= 1000.0 && c->speed_of_sound_mps <= 2000.0))
+    return fail(SUPRA_E_PARAM, "speed_of_sound must be in [1000, 2000] m/s (S:126)");
+  if (!std::isfinite(c->t0_s)) return fail(SUPRA_E_PARAM, "t0 must be finite");
+  if (c->num_lines_x < 1 || c->num_lines_y < 1) return fail(SUPRA_E_PARAM, "num_lines must be >= 1");
+  if (!c->line_origin_mm || !c->line_direction || !c->line_event)
+    return fail(SUPRA_E_STRUCT, "line arrays must not be NULL");
+  if (!(c->f_number > 0)) return fail(SUPRA_E_PARAM, "f_number must be > 0 (S:126)");
+  if (c->window < SUPRA_WIN_RECT || c->window > SUPRA_WIN_HAMMING) return fail(SUPRA_E_PARAM, "window");
+  if (c->normalize != SUPRA_NORM_COUNT && c->normalize != SUPRA_NORM_NONE) return fail(SUPRA_E_PARAM, "normalize");
+  if (c->fir_taps < 1 || c->fir_taps > 129 || c->fir_taps % 2 == 0)
+    return fail(SUPRA_E_PARAM, "fir_taps must be odd in [1, 129] (S:196)");
+  if (c->decimation != 1) return fail(SUPRA_E_PARAM, "decimation must be 1 in this version");
+  double fd = c->demod_frequency_hz, bw = c->demod_bandwidth_hz;
+  if (!(bw > 0) || !(fd - bw / 2 > 0) || !(fd + bw / 2 < c->sample_frequency_hz / 2))
+    return fail(SUPRA_E_PARAM, "demodulation band must lie inside (0, fs/2) (S:188)");
+  if (!(c->dynamic_range_db > 0)) return fail(SUPRA_E_PARAM, "dynamic_range_db must be > 0 (S:247)");
+  if (c->reference_mode != SUPRA_REF_FRAME_MAX && c->reference_mode != SUPRA_REF_FIXED)
+    return fail(SUPRA_E_PARAM, "reference_mode");
+  if (c->reference_mode == SUPRA_REF_FIXED && !(c->reference_value > 0))
+    return fail(SUPRA_E_PARAM, "fixed reference must be > 0 (S:247)");
+  if (c->line_output_type != SUPRA_T_F32 && c->line_output_type != SUPRA_T_U8)
+    return fail(SUPRA_E_PARAM, "line_output_type must be F32 or U8");
+  if (c->sc_output_type != SUPRA_T_F32 && c->sc_output_type != SUPRA_T_U8)
+    return fail(SUPRA_E_PARAM, "sc_output_type must be F32 or U8");
+  if (c->sc_kind < SUPRA_SC_LINEAR_2D || c->sc_kind > SUPRA_SC_PYRAMID_3D) return fail(SUPRA_E_PARAM, "sc_kind");
+  for (int i = 0; i < 3; i++) {
+    if (c->out_dims[i] < 1) return fail(SUPRA_E_PARAM, "out_dims must be >= 1");
+    if (!(c->out_spacing_mm[i] > 0)) return fail(SUPRA_E_PARAM, "out_spacing must be > 0 (S:296)");
+    if (!std::isfinite(c->out_origin_mm[i])) return fail(SUPRA_E_PARAM, "out_origin must be finite");
+  }
+  if (c->max_frames_per_call < 1) return fail(SUPRA_E_PARAM, "max_frames_per_call must be >= 1");
+  const int L = c->num_lines_x * c->num_lines_y;
+  for (int l = 0; l < L; l++)
+    if (c->line_event[l] < 0 || c->line_event[l] >= c->num_events)
+      return fail(SUPRA_E_STRUCT, "line_event[%d] = %d out of [0, %d)", l, c->line_event[l], c->num_events);
+  for (int l = 0; l < L; l++) {
+    const double* d = c->line_direction + 3 * l;
+    double n = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (!(std::fabs(n - 1.0) <= 1e-9)) return fail(SUPRA_E_PARAM, "line_direction[%d] not unit (S:37)", l);
+    if (c->line_origin_mm[3 * l + 2] != 0.0) return fail(SUPRA_E_PARAM, "line origins must lie on the array face z = 0");
+  }
+  // geometry must match the scan-conversion inverse map
+  const double tol = 1e-9;
+  if (c->sc_kind == SUPRA_SC_LINEAR_2D) {
+    if (c->num_lines_y != 1 || c->num_lines_x < 2) return fail(SUPRA_E_PARAM, "LINEAR_2D needs 1 x (>=2) lines");
+    if (c->out_dims[1] != 1) return fail(SUPRA_E_PARAM, "2D output needs out_dims[1] = 1");
+    double x0 = c->line_origin_mm[0], xL = c->line_origin_mm[3 * (L - 1)];
+    if (!(xL > x0)) return fail(SUPRA_E_PARAM, "LINEAR_2D origins must increase");
+    double span = xL - x0;
+    for (int l = 0; l < L; l++) {
+      const double* o = c->line_origin_mm + 3 * l;
+      const double* d = c->line_direction + 3 * l;
+      double xe = x0 + span * l / (L - 1);
+      if (std::fabs(o[0] - xe) > tol * std::max(1.0, span) || o[1] != 0.0)
+        return fail(SUPRA_E_PARAM, "LINEAR_2D origins must be evenly spaced on the x axis");
+      if (std::fabs(d[0]) > tol || std::fabs(d[1]) > tol || std::fabs(d[2] - 1.0) > tol)
+        return fail(SUPRA_E_PARAM, "LINEAR_2D directions must be (0,0,1)");
+    }
+  } else {
+    const bool is3d = c->sc_kind == SUPRA_SC_PYRAMID_3D;
+    if (!(c->fov_x_deg > 0 && c->fov_x_deg < 180)) return fail(SUPRA_E_PARAM, "fov_x must be in (0, 180) (S:64)");
+    if (is3d && !(c->fov_y_deg > 0 && c->fov_y_deg < 180)) return fail(SUPRA_E_PARAM, "fov_y must be in (0, 180) (S:64)");
+    if (c->num_lines_x < 2) return fail(SUPRA_E_PARAM, "phased layouts need >= 2 lines in x");
+    if (!is3d && (c->num_lines_y != 1 || c->out_dims[1] != 1)) return fail(SUPRA_E_PARAM, "SECTOR_2D needs 1 line row and out_dims[1] = 1");
+    if (is3d && c->num_lines_y < 2) return fail(SUPRA_E_PARAM, "PYRAMID_3D needs >= 2 lines in y");
+    const double fx = c->fov_x_deg * kPi / 180.0, fy = c->fov_y_deg * kPi / 180.0;
+    for (int l = 0; l < L; l++) {
+      int lx = l % c->num_lines_x, ly = l / c->num_lines_x;
+      double tx = (lx - (c->num_lines_x - 1) / 2.0) * (fx / (c->num_lines_x - 1));
+      double ty = is3d ? (ly - (c->num_lines_y - 1) / 2.0) * (fy / (c->num_lines_y - 1)) : 0.0;
+      double e[3] = {std::sin(tx), std::cos(tx) * std::sin(ty), std::cos(tx) * std::cos(ty)};
+      const double* o = c->line_origin_mm + 3 * l;
+      const double* d = c->line_direction + 3 * l;
+      if (o[0] != 0.0 || o[1] != 0.0) return fail(SUPRA_E_PARAM, "phased line origins must be 0");
+      for (int i = 0; i < 3; i++)
+        if (std::fabs(d[i] - e[i]) > tol)
+          return fail(SUPRA_E_PARAM, "line_direction[%d] off the uniform angle grid (reading #13/#14)", l);
+    }
+  }
+  return SUPRA_OK;
+}
+
+// ---- DAS tables ------------------------------------------------------
+supra_status build_das_tables(supra_bf* h) {
+  const supra_bf_config& c = h->cfg;
+  const int L = h->L, C = h->C, S = h->S;
+  const double dr = h->dr_mm, sc = h->s_per_mm, F = c.f_number;
+  // line groups: lines with bitwise-identical origins share an aperture table
+  std::map<std::vector<double>, int> gid;
+  std::vector<int32_t> line_group(L);
+  std::vector<const double*> g_origin;
+  for (int l = 0; l < L; l++) {
+    std::vector<double> key(c.line_origin_mm + 3 * l, c.line_origin_mm + 3 * l + 3);
+    auto it = gid.find(key);
+    if (it == gid.end()) {
+      it = gid.emplace(key, (int)g_origin.size()).first;
+      g_origin.push_back(c.line_origin_mm + 3 * l);
+    }
+    line_group[l] = it->second;
+  }
+  const int G = (int)g_origin.size();
+  h->G = G;
+  std::vector<std::vector<DasEntry>> groups(G);
+  size_t maxn = 0;
+  for (int g = 0; g < G; g++) {
+    const double* o = g_origin[g];
+    auto& v = groups[g];
+    for (int ch = 0; ch < C; ch++) {
+      double e[3];
+      elem_pos(c, ch, e);
+      double rho = std::hypot(e[0] - o[0], e[1] - o[1]);
+      int ke = k_enter(F, rho, dr, S);
+      if (ke >= S) continue;  // never in the aperture within the record
+      DasEntry d{};
+      double q0 = (o[0] - e[0]) * sc, q1 = (o[1] - e[1]) * sc, q2 = (o[2] - e[2]) * sc;
+      d.qx = (float)q0;
+      d.qy = (float)q1;
+      d.qz = (float)q2;
+      d.A = (float)(q0 * q0 + q1 * q1 + q2 * q2);
+      d.cu = (float)(4.0 * F * rho * sc);
+      d.elem = ch;
+      d.kenter = ke;
+      v.push_back(d);
+    }
+    std::stable_sort(v.begin(), v.end(),
+                     [](const DasEntry& a, const DasEntry& b) { return a.kenter < b.kenter; });
+    maxn = std::max(maxn, v.size());
+  }
+  const int per = (int)std::max<size_t>(32, (maxn + 31) / 32 * 32);
+  h->entries_per_group = per;
+  h->ntiles = (S + kTileK - 1) / kTileK;
+  std::vector<DasEntry> flat((size_t)G * per);
+  std::vector<int32_t> ntile((size_t)G * h->ntiles);
+  for (int g = 0; g < G; g++) {
+    for (int j = 0; j < per; j++) {
+      DasEntry d{};
+      if (j < (int)groups[g].size()) d = groups[g][j];
+      else { d.kenter = 0x7fffffff; }
+      flat[(size_t)g * per + j] = d;
+    }
+    for (int t = 0; t < h->ntiles; t++) {
+      int klast = std::min((t + 1) * kTileK, S) - 1;
+      int n = 0;
+      for (auto& d : groups[g]) n += (d.kenter <= klast);
+      ntile[(size_t)g * h->ntiles + t] = n;
+    }
+  }
+  std::vector<float4> dirs(L);
+  std::vector<int32_t> ev(c.line_event, c.line_event + L);
+  for (int l = 0; l < L; l++)
+    dirs[l] = make_float4((float)c.line_direction[3 * l], (float)c.line_direction[3 * l + 1],
+                          (float)c.line_direction[3 * l + 2], 0.f);
+  // FIR: Hamming-windowed sinc low-pass, cutoff bw/2, DC gain 1 (S:227,
+  // reading #16), rotated to the complex band-pass g_j = h_j e^{+i w j}
+  // (reading #18), w = 2 pi f_d / fs.
+  const int T = c.fir_taps, P = (T - 1) / 2;
+  const double fc = c.demod_bandwidth_hz / 2.0, fs = c.sample_frequency_hz;
+  std::vector<double> hd(T);
+  double sum = 0;
+  for (int j = -P; j <= P; j++) {
+    double s = (j == 0) ? 2.0 * fc / fs : std::sin(2.0 * kPi * fc * j / fs) / (kPi * j);
+    double w = (T > 1) ? 0.54 + 0.46 * std::cos(2.0 * kPi * j / (T - 1)) : 1.0;
+    hd[j + P] = w * s;
+    sum += w * s;
+  }
+  std::vector<float2> fir(T);
+  const double om = 2.0 * kPi * c.demod_frequency_hz / fs;
+  for (int j = -P; j <= P; j++) {
+    double hj = hd[j + P] / sum;
+    fir[j + P] = make_float2((float)(hj * std::cos(om * j)), (float)(hj * std::sin(om * j)));
+  }
+  cudaError_t e;
+  if ((e = upload(&h->d_line_group, line_group)) != cudaSuccess ||
+      (e = upload(&h->d_entries, flat)) != cudaSuccess || (e = upload(&h->d_ntile, ntile)) != cudaSuccess ||
+      (e = upload(&h->d_line_dir, dirs)) != cudaSuccess || (e = upload(&h->d_line_event, ev)) != cudaSuccess ||
+      (e = upload(&h->d_fir, fir)) != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "table upload: %s",
+                cudaGetErrorString(e));
+  // Work accounting for the bench: taps and referenced input bytes.  For a
+  // (line, entry) the referenced samples over k in [k_enter, S) are the
+  // contiguous range [floor tau(k_enter), floor tau(S-1) + 1] (d tau / dk in
+  // [0, 1]), clipped to [0, S); multi-line events take the union.
+  int64_t taps = 0;
+  std::vector<std::vector<std::pair<long, long>>> iv((size_t)h->E * C);
+  for (int l = 0; l < L; l++) {
+    const double* o = c.line_origin_mm + 3 * l;
+    const double* d = c.line_direction + 3 * l;
+    for (auto& de : groups[line_group[l]]) {
+      taps += S - de.kenter;
+      double e3[3];
+      elem_pos(c, de.elem, e3);
+      long a = (long)std::floor(tau_d(o, d, e3, de.kenter, dr, fs, c.speed_of_sound_mps, c.t0_s));
+      long b = (long)std::floor(tau_d(o, d, e3, S - 1, dr, fs, c.speed_of_sound_mps, c.t0_s)) + 1;
+      a = std::max(a, 0L);
+      b = std::min(b, (long)S - 1);
+      if (b >= a) iv[(size_t)c.line_event[l] * C + de.elem].push_back({a, b});
+    }
+  }
+  int64_t ref = 0;
+  for (auto& v : iv) {
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    long ca = v[0].first, cb = v[0].second;
+    for (size_t i = 1; i < v.size(); i++) {
+      if (v[i].first <= cb + 1) cb = std::max(cb, v[i].second);
+      else { ref += cb - ca + 1; ca = v[i].first; cb = v[i].second; }
+    }
+    ref += cb - ca + 1;
+  }
+  h->info[3] = ref * 2;
+  h->info[4] = taps;
+  return SUPRA_OK;
+}
+
+// ---- scan-conversion tables (reading #21/#22; same definition as the
+// analytic inverse map written out in DESIGN.md) -------------------------
+void sc_axis(double u, int L, int32_t* i0, double* f) {
+  if (L == 1) { *i0 = 0; *f = 0.0; return; }
+  double fl = std::floor(u);
+  int32_t i = (int32_t)fl;
+  if (i > L - 2) i = L - 2;
+  *i0 = i;
+  *f = u - i;
+}
+
+supra_status build_sc_tables(supra_bf* h) {
+  const supra_bf_config& c = h->cfg;
+  const int nx = c.out_dims[0], ny = c.out_dims[1], nz = c.out_dims[2];
+  const int Lx = c.num_lines_x, Ly = c.num_lines_y, S = h->S;
+  const double dr = h->dr_mm;
+  int64_t nvalid = 0;
+  cudaError_t e = cudaSuccess;
+  if (c.sc_kind == SUPRA_SC_LINEAR_2D) {
+    const double x0 = c.line_origin_mm[0], xL = c.line_origin_mm[3 * (Lx - 1)];
+    const double pitch = (xL - x0) / (Lx - 1);
+    h->h_ax.resize(nx);
+    h->h_az.resize(nz);
+    int64_t vx = 0, vz = 0;
+    for (int ix = 0; ix < nx; ix++) {
+      double X = c.out_origin_mm[0] + ix * c.out_spacing_mm[0];
+      double u = (X - x0) / pitch;
+      int32_t i0;
+      double f;
+      sc_axis(u, Lx, &i0, &f);
+      bool ok = u >= 0.0 && u <= Lx - 1;
+      h->h_ax[ix] = ScAxis{ok ? i0 : -1, (float)f};
+      vx += ok;
+    }
+    for (int iz = 0; iz < nz; iz++) {
+      double Z = c.out_origin_mm[2] + iz * c.out_spacing_mm[2];
+      double v = Z / dr;
+      int32_t k0;
+      double f;
+      sc_axis(v, S, &k0, &f);
+      bool ok = v >= 0.0 && v <= S - 1;
+      h->h_az[iz] = ScAxis{ok ? k0 : -1, (float)f};
+      vz += ok;
+    }
+    nvalid = vx * vz;
+    if ((e = upload(&h->d_ax, h->h_ax)) != cudaSuccess || (e = upload(&h->d_az, h->h_az)) != cudaSuccess)
+      return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "sc upload: %s",
+                  cudaGetErrorString(e));
+    h->info[5] = (int64_t)(nx + nz) * sizeof(ScAxis);
+  } else {
+    const bool is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
+    const double fovx = c.fov_x_deg * kPi / 180.0, fovy = c.fov_y_deg * kPi / 180.0;
+    const double dthx = fovx / (Lx - 1), dthy = is3d ? fovy / (Ly - 1) : 1.0;
+    h->h_rows.assign((size_t)nz * ny, ScRow{0, 0, 0});
+    h->h_ent.clear();
+    std::vector<ScEntry> rowbuf(nx);
+    std::vector<char> okbuf(nx);
+    for (int iz = 0; iz < nz; iz++) {
+      const double Z = c.out_origin_mm[2] + iz * c.out_spacing_mm[2];
+      for (int iy = 0; iy < ny; iy++) {
+        const double Y = c.out_origin_mm[1] + iy * c.out_spacing_mm[1];
+        int lo = -1, hi = -1;
+        for (int ix = 0; ix < nx; ix++) {
+          const double X = c.out_origin_mm[0] + ix * c.out_spacing_mm[0];
+          double ux, uy = 0.0, v;
+          if (!is3d) {
+            ux = std::atan2(X, Z) / dthx + (Lx - 1) / 2.0;
+            v = std::sqrt(X * X + Z * Z) / dr;
+          } else {
+            uy = std::atan2(Y, Z) / dthy + (Ly - 1) / 2.0;
+            ux = std::atan2(X, std::sqrt(Y * Y + Z * Z)) / dthx + (Lx - 1) / 2.0;
+            v = std::sqrt(X * X + Y * Y + Z * Z) / dr;
+          }
+          bool ok = (ux >= 0.0 && ux <= Lx - 1) && (v >= 0.0 && v <= S - 1);
+          if (is3d) ok = ok && (uy >= 0.0 && uy <= Ly - 1);
+          int32_t i0x, i0y, k0;
+          double fx, fy, fz;
+          sc_axis(ux, Lx, &i0x, &fx);
+          sc_axis(uy, is3d ? Ly : 1, &i0y, &fy);
+          sc_axis(v, S, &k0, &fz);
+          okbuf[ix] = ok;
+          rowbuf[ix] = ScEntry{ok ? (i0y * Lx + i0x) * S + k0 : -1, (float)fx, (float)fy, (float)fz};
+          if (ok) {
+            if (lo < 0) lo = ix;
+            hi = ix + 1;
+            nvalid++;
+          }
+        }
+        ScRow& r = h->h_rows[(size_t)iz * ny + iy];
+        if (lo >= 0) {
+          r = ScRow{lo, hi, (int64_t)h->h_ent.size()};
+          h->h_ent.insert(h->h_ent.end(), rowbuf.begin() + lo, rowbuf.begin() + hi);
+        } else {
+          r = ScRow{0, 0, (int64_t)h->h_ent.size()};
+        }
+      }
+    }
+    if ((e = upload(&h->d_rows, h->h_rows)) != cudaSuccess || (e = upload(&h->d_ent, h->h_ent)) != cudaSuccess)
+      return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "sc upload: %s",
+                  cudaGetErrorString(e));
+    h->info[5] = (int64_t)h->h_rows.size() * sizeof(ScRow) + (int64_t)h->h_ent.size() * sizeof(ScEntry);
+  }
+  h->info[6] = nvalid;
+  h->info[7] = 1;
+  return SUPRA_OK;
+}
+
+bool is_device_ptr(const void* p, int dev) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.device == dev;
+}
+
+supra_status check_launch(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SUPRA_OK;
+  return fail(SUPRA_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void fill_log(const supra_bf* h, int& fixed, float& k1, float& k0) {
+  fixed = h->cfg.reference_mode == SUPRA_REF_FIXED;
+  double kk1 = 20.0 * std::log10(2.0) / h->cfg.dynamic_range_db;
+  k1 = (float)kk1;
+  k0 = fixed ? (float)(1.0 - kk1 * std::log2(h->cfg.reference_value)) : 1.0f;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* supra_bf_last_error(void) { return g_err.c_str(); }
+
+supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
+  g_err.clear();
+  if (!out) return fail(SUPRA_E_STRUCT, "out is NULL");
+  *out = nullptr;
+  supra_status s = validate(cfg);
+  if (s != SUPRA_OK) return s;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(SUPRA_E_CUDA, "no CUDA device available (there is no CPU fallback)");
+  }
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(SUPRA_E_STRUCT, "device %d not present", cfg->device);
+  DeviceGuard dg(cfg->device);
+  if (!dg.ok) return fail(SUPRA_E_CUDA, "cudaSetDevice(%d) failed", cfg->device);
+  if ((int64_t)cfg->num_lines_x * cfg->num_lines_y * cfg->samples_per_channel >= (1LL << 31))
+    return fail(SUPRA_E_PARAM, "L * samples_per_channel must be < 2^31");
+  supra_bf* h = new supra_bf();
+  h->cfg = *cfg;  // the line arrays are read by the builders below, then dropped
+  h->L = cfg->num_lines_x * cfg->num_lines_y;
+  h->C = cfg->elements_x * cfg->elements_y;
+  h->S = cfg->samples_per_channel;
+  h->E = cfg->num_events;
+  h->dr_mm = 1000.0 * cfg->speed_of_sound_mps / (2.0 * cfg->sample_frequency_hz);
+  h->s_per_mm = cfg->sample_frequency_hz / (1000.0 * cfg->speed_of_sound_mps);
+  s = build_das_tables(h);
+  if (s == SUPRA_OK) s = build_sc_tables(h);
+  h->cfg.line_origin_mm = nullptr;
+  h->cfg.line_direction = nullptr;
+  h->cfg.line_event = nullptr;
+  if (s != SUPRA_OK) {
+    free_all(h);
+    delete h;
+    return s;
+  }
+  // DAS launch shape
+  const int maxF = cfg->max_frames_per_call;
+  h->frames_per_cta = das_max_frames_per_cta(h->S, cfg->fir_taps, maxF);
+  if (const char* ev = std::getenv("SUPRA_BF_FRAMES_PER_CTA")) {
+    int v = std::atoi(ev);
+    if (v == 1 || v == 2 || v == 4 || v == 8) h->frames_per_cta = std::min(v, 8);
+  }
+  h->das_smem = das_smem_bytes(h->frames_per_cta, h->S, cfg->fir_taps);
+  cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
+  if (e == cudaSuccess && cfg->reference_mode == SUPRA_REF_FRAME_MAX && cfg->line_output_type == SUPRA_T_U8)
+    e = cudaMalloc((void**)&h->d_env, sizeof(float) * (size_t)maxF * h->L * h->S);
+  if (e != cudaSuccess) {
+    free_all(h);
+    delete h;
+    return fail(SUPRA_E_RESOURCE, "scratch allocation: %s", cudaGetErrorString(e));
+  }
+  h->info[0] = (cfg->reference_mode == SUPRA_REF_FRAME_MAX) ? 2 : 1;
+  h->info[1] = h->frames_per_cta;
+  h->info[2] = kTileK;
+  *out = h;
+  return SUPRA_OK;
+}
+
+void supra_bf_destroy(supra_bf_t h) {
+  if (!h) return;
+  DeviceGuard dg(h->cfg.device);
+  cudaDeviceSynchronize();
+  free_all(h);
+  delete h;
+}
+
+supra_status supra_bf_info(supra_bf_t h, int64_t* info8) {
+  if (!h || !info8) return fail(SUPRA_E_STRUCT, "NULL argument");
+  std::memcpy(info8, h->info, sizeof h->info);
+  return SUPRA_OK;
+}
+
+static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float* rf, void* line_img,
+                            cudaStream_t st) {
+  const supra_bf_config& c = h->cfg;
+  DasArgs a{};
+  a.raw = (const int16_t*)raw;
+  a.F = frames;
+  a.E = h->E;
+  a.C = h->C;
+  a.S = h->S;
+  a.L = h->L;
+  a.ntiles = h->ntiles;
+  a.entries_per_group = h->entries_per_group;
+  a.line_group = h->d_line_group;
+  a.entries = h->d_entries;
+  a.ntile = h->d_ntile;
+  a.line_dir = h->d_line_dir;
+  a.line_event = h->d_line_event;
+  a.t0fs = (float)(c.t0_s * c.sample_frequency_hz);
+  a.win_a = c.window == SUPRA_WIN_HANN ? 0.5f : (c.window == SUPRA_WIN_HAMMING ? 0.54f : 1.0f);
+  a.win_b = c.window == SUPRA_WIN_HANN ? 0.5f : (c.window == SUPRA_WIN_HAMMING ? 0.46f : 0.0f);
+  a.normalize = c.normalize;
+  a.rf = rf;
+  a.do_epilogue = line_img != nullptr;
+  a.fir = h->d_fir;
+  a.fir_taps = c.fir_taps;
+  fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
+  a.y_type = c.line_output_type;
+  if (line_img) {
+    if (a.ref_fixed) {
+      a.y_out = line_img;
+    } else {
+      a.env_out = (c.line_output_type == SUPRA_T_F32) ? (float*)line_img : h->d_env;
+      a.frame_max = h->d_frame_max;
+      cudaError_t e = cudaMemsetAsync(h->d_frame_max, 0, sizeof(unsigned) * frames, st);
+      if (e != cudaSuccess) return check_launch(e, "memset frame_max");
+    }
+  }
+  supra_status s = check_launch(launch_das(a, h->frames_per_cta, h->das_smem, st), "das kernel");
+  if (s != SUPRA_OK || !line_img || a.ref_fixed) return s;
+  FinalizeArgs fa{};
+  fa.env = a.env_out;
+  fa.per_frame = (long long)h->L * h->S;
+  fa.F = frames;
+  fa.frame_max = h->d_frame_max;
+  fa.DR_k = a.log_k1;
+  fa.y_out = line_img;
+  fa.y_type = c.line_output_type;
+  return check_launch(launch_finalize(fa, st), "finalize kernel");
+}
+
+supra_status supra_bf_beamform(supra_bf_t h, const void* raw, int32_t frames, float* rf, void* line_img,
+                               void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (!rf && !line_img) return fail(SUPRA_E_STRUCT, "both rf and line_img are NULL");
+  if (frames == 0) return SUPRA_OK;
+  if (!raw || ((uintptr_t)raw & 15)) return fail(SUPRA_E_STRUCT, "raw must be a 16-byte aligned device pointer");
+  DeviceGuard dg(h->cfg.device);
+  const int dev = h->cfg.device;
+  if (!is_device_ptr(raw, dev)) return fail(SUPRA_E_STRUCT, "raw is not device memory of device %d", dev);
+  if (rf && !is_device_ptr(rf, dev)) return fail(SUPRA_E_STRUCT, "rf is not device memory of device %d", dev);
+  if (line_img && !is_device_ptr(line_img, dev))
+    return fail(SUPRA_E_STRUCT, "line_img is not device memory of device %d", dev);
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return fail(SUPRA_E_CUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
+  return run_das(h, raw, frames, rf, line_img, (cudaStream_t)stream);
+}
+
+supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames, void* line_img, void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (!rf || !line_img) return fail(SUPRA_E_STRUCT, "rf and line_img must not be NULL");
+  if (frames == 0) return SUPRA_OK;
+  DeviceGuard dg(h->cfg.device);
+  const int dev = h->cfg.device;
+  if (!is_device_ptr(rf, dev) || !is_device_ptr(line_img, dev))
+    return fail(SUPRA_E_STRUCT, "rf / line_img are not device memory of device %d", dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const supra_bf_config& c = h->cfg;
+  EnvArgs a{};
+  a.rf = rf;
+  a.F = frames;
+  a.L = h->L;
+  a.S = h->S;
+  a.fir = h->d_fir;
+  a.fir_taps = c.fir_taps;
+  fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
+  a.y_type = c.line_output_type;
+  if (a.ref_fixed) {
+    a.y_out = line_img;
+  } else {
+    a.env_out = (c.line_output_type == SUPRA_T_F32) ? (float*)line_img : h->d_env;
+    a.frame_max = h->d_frame_max;
+    cudaError_t e = cudaMemsetAsync(h->d_frame_max, 0, sizeof(unsigned) * frames, st);
+    if (e != cudaSuccess) return check_launch(e, "memset frame_max");
+  }
+  supra_status s = check_launch(launch_envlog(a, st), "envlog kernel");
+  if (s != SUPRA_OK || a.ref_fixed) return s;
+  FinalizeArgs fa{};
+  fa.env = a.env_out;
+  fa.per_frame = (long long)h->L * h->S;
+  fa.F = frames;
+  fa.frame_max = h->d_frame_max;
+  fa.DR_k = a.log_k1;
+  fa.y_out = line_img;
+  fa.y_type = c.line_output_type;
+  return check_launch(launch_finalize(fa, st), "finalize kernel");
+}
+
+supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t frames, void* img, uint8_t* mask,
+                                  void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (!line_img || !img) return fail(SUPRA_E_STRUCT, "line_img and img must not be NULL");
+  if (frames == 0) return SUPRA_OK;
+  DeviceGuard dg(h->cfg.device);
+  const int dev = h->cfg.device;
+  if (!is_device_ptr(line_img, dev) || !is_device_ptr(img, dev) || (mask && !is_device_ptr(mask, dev)))
+    return fail(SUPRA_E_STRUCT, "line_img / img / mask are not device memory of device %d", dev);
+  const supra_bf_config& c = h->cfg;
+  ScArgs a{};
+  a.line_img = line_img;
+  a.in_type = c.line_output_type;
+  a.F = frames;
+  a.Lx = c.num_lines_x;
+  a.Ly = c.num_lines_y;
+  a.S = h->S;
+  a.nx = c.out_dims[0];
+  a.ny = c.out_dims[1];
+  a.nz = c.out_dims[2];
+  a.img = img;
+  a.out_type = c.sc_output_type;
+  a.mask = mask;
+  a.ax = h->d_ax;
+  a.az = h->d_az;
+  a.rows = h->d_rows;
+  a.ent = h->d_ent;
+  a.is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c.sc_kind == SUPRA_SC_LINEAR_2D) return check_launch(launch_sc_linear(a, st), "sc_linear kernel");
+  return check_launch(launch_sc_table(a, st), "sc_table kernel");
+}
+
+supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t* valid, int32_t* idx) {
+  if (!h || !valid || !idx) return fail(SUPRA_E_STRUCT, "NULL argument");
+  const supra_bf_config& c = h->cfg;
+  const int nx = c.out_dims[0], ny = c.out_dims[1], nz = c.out_dims[2], S = h->S, Lx = c.num_lines_x;
+  size_t n = 0;
+  for (int iz = 0; iz < nz; iz++)
+    for (int iy = 0; iy < ny; iy++)
+      for (int ix = 0; ix < nx; ix++, n++) {
+        idx[3 * n] = idx[3 * n + 1] = idx[3 * n + 2] = 0;
+        if (c.sc_kind == SUPRA_SC_LINEAR_2D) {
+          const ScAxis &ax = h->h_ax[ix], &az = h->h_az[iz];
+          valid[n] = ax.i0 >= 0 && az.i0 >= 0;
+          idx[3 * n] = ax.i0;
+          idx[3 * n + 2] = az.i0;
+        } else {
+          const ScRow& r = h->h_rows[(size_t)iz * ny + iy];
+          valid[n] = 0;
+          if (ix >= r.xlo && ix < r.xhi) {
+            int32_t b = h->h_ent[r.off + (ix - r.xlo)].base;
+            if (b >= 0) {
+              valid[n] = 1;
+              idx[3 * n + 2] = b % S;
+              int li = b / S;
+              idx[3 * n] = li % Lx;
+              idx[3 * n + 1] = li / Lx;
+            }
+          }
+        }
+      }
+  return SUPRA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// internal.h -- types shared by the host library (host.cpp) and the sm_100a
+// kernels (das.cu, epilogue.cu, scanconv.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "supra_bf.h"
+
+namespace supra {
+
+// Depth tile of the DAS kernel: one output sample per consumer thread.
+constexpr int kTileK = 256;
+// Staged window per (entry, frame): tile + delay spread margin, in samples.
+// floor tau(k1) - floor tau(k0) <= k1 - k0 + 1 (d tau/dk in [0,1]); the
+// window adds 2 + 3 samples of safety margin and up to 7 + 7 of 16-byte
+// alignment on either end: <= kTileK + 20.
+constexpr int kWin = kTileK + 24;
+// Stages in the bulk-copy ring.
+constexpr int kStages = 4;
+// Producer lanes == bulk copies per stage (entries-per-stage x frames-per-CTA).
+constexpr int kCopiesPerStage = 32;
+
+// One receive-aperture entry of a line group (lines sharing an origin),
+// sorted by k_enter.  Lengths in "sample units" (mm * fs / (1000 c)), in
+// which the focal depth of output sample k is h = k/2.
+struct __align__(16) DasEntry {
+  float qx, qy, qz;  // (line origin - element position) in samples
+  float A;           // |q|^2, rounded from binary64
+  float cu;          // 4 F rho_s:  u = rho/R = cu / k  (R = z/(2F))
+  int32_t elem;      // channel index
+  int32_t kenter;    // first k with (2F) rho <= k dr (binary64 predicate); >= S: never
+  int32_t pad;
+};
+
+struct DasArgs {
+  const int16_t* raw;      // [F][E][C][S]
+  int F, E, C, S, L;
+  int ntiles;              // ceil(S / kTileK)
+  int entries_per_group;   // padded to a multiple of 32
+  const int32_t* line_group;   // [L]
+  const DasEntry* entries;     // [G][entries_per_group]
+  const int32_t* ntile;        // [G][ntiles]: entries with kenter <= last k of tile
+  const float4* line_dir;      // [L] (dx, dy, dz, 0)
+  const int32_t* line_event;   // [L]
+  float t0fs;                  // t0 * fs (samples)
+  float win_a, win_b;          // w = a + b cos(pi u)
+  int normalize;               // 0 count, 1 none
+  // outputs
+  float* rf;                   // [F][L][S] or null
+  int do_epilogue;             // 1: FIR + envelope (+ log) epilogue
+  const float2* fir;           // [T] complex taps g_j = h_j e^{+i w j}, j = -P..P
+  int fir_taps;
+  int ref_fixed;               // 1: y written directly; 0: env written + frame max
+  float log_k1, log_k0;        // y = k1 log2(env) + k0 (fixed reference)
+  float* env_out;              // [F][L][S] f32 (frame-max mode)
+  void* y_out;                 // [F][L][S] (fixed mode)
+  int y_type;                  // SUPRA_T_F32 / SUPRA_T_U8
+  unsigned* frame_max;         // [F] float bits (frame-max mode)
+};
+
+struct EnvArgs {  // standalone epilogue on an RF buffer
+  const float* rf;
+  int F, L, S;
+  const float2* fir;
+  int fir_taps;
+  int ref_fixed;
+  float log_k1, log_k0;
+  float* env_out;
+  void* y_out;
+  int y_type;
+  unsigned* frame_max;
+};
+
+struct FinalizeArgs {  // frame-max reference: env -> y
+  const float* env;    // [F][L*S]
+  long long per_frame; // L*S
+  int F;
+  const unsigned* frame_max;
+  float DR_k;          // 20 log10(2) / DR
+  void* y_out;
+  int y_type;
+};
+
+// Linear (separable) scan conversion table entries.
+struct ScAxis {
+  int32_t i0;   // -1: invalid
+  float f;
+};
+
+// Sector / pyramid: per output row (iz, iy) the valid x range and the
+// offset of its first entry; entries hold the line-image offset of the
+// (i0x, i0y, k0) corner (-1: invalid) and the three fractions.
+struct ScRow {
+  int32_t xlo, xhi;
+  int64_t off;
+};
+struct __align__(16) ScEntry {
+  int32_t base;   // (i0y*Lx + i0x)*S + k0, or -1
+  float fx, fy, fz;
+};
+
+struct ScArgs {
+  const void* line_img;  // [F][Ly][Lx][S]
+  int in_type;
+  int F, Lx, Ly, S;
+  int nx, ny, nz;
+  void* img;             // [F][nz][ny][nx]
+  int out_type;
+  uint8_t* mask;         // [nz][ny][nx] or null
+  // linear
+  const ScAxis* ax;      // [nx]
+  const ScAxis* az;      // [nz]
+  // table
+  const ScRow* rows;     // [nz*ny]
+  const ScEntry* ent;
+  int is3d;
+};
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_das(const DasArgs& a, int frames_per_cta, size_t smem_bytes, cudaStream_t st);
+size_t das_smem_bytes(int frames_per_cta, int S, int fir_taps);
+int das_max_frames_per_cta(int S, int fir_taps, int F);
+cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st);
+cudaError_t launch_sc_table(const ScArgs& a, cudaStream_t st);
+
+}  // namespace supra
