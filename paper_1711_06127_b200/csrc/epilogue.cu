@@ -1,29 +1,51 @@
 // epilogue.cu -- standalone IQ envelope + log compression on an RF buffer
 // (supra_bf_envelope_log) and the frame-max finalisation shared with the
 // fused path.
+#include <algorithm>
+
 #include "epilogue.cuh"
 
 namespace supra {
 
 // One CTA per (line, frame): the RF line is staged in shared memory with
-// zeroed FIR halos, then the same epilogue as the fused DAS path runs.
+// zeroed FIR halos; each thread produces env (or y) for strided samples.
 __global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int S = a.S, T = a.fir_taps, P = (T - 1) / 2;
-  float2* fir = (float2*)smem_raw;
-  float* rfs = (float*)(smem_raw + ((sizeof(float2) * T + 15) & ~size_t(15)));
-  unsigned* smax = (unsigned*)(rfs + S + 2 * P);
+  const int S = a.S, P = (a.fir_taps - 1) / 2;
+  float* cs = (float*)smem_raw;                  // c[0..P], s[0..P]
+  float* rfs = cs + 2 * (kMaxHalfTaps + 1);
+  __shared__ unsigned smax;
   const int line = blockIdx.x, f = blockIdx.y;
   const float* src = a.rf + ((size_t)f * a.L + line) * S;
-  for (int i = threadIdx.x; i < T; i += blockDim.x) fir[i] = a.fir[i];
+  for (int i = threadIdx.x; i <= P; i += blockDim.x) {
+    cs[i] = a.fir[i + P].x;
+    cs[kMaxHalfTaps + 1 + i] = a.fir[i + P].y;
+  }
   for (int i = threadIdx.x; i < S + 2 * P; i += blockDim.x) {
     int k = i - P;
     rfs[i] = (k >= 0 && k < S) ? src[k] : 0.f;
   }
-  if (threadIdx.x < 8) smax[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) smax = 0u;
   __syncthreads();
-  fused_epilogue<1>(rfs, fir, T, S, a.L, line, f, a.F, a.ref_fixed, a.log_k1, a.log_k0, a.env_out,
-                    a.y_out, a.y_type, a.frame_max, smax);
+  float m = 0.f;
+  for (int k = threadIdx.x; k < S; k += blockDim.x) {
+    const float env = envelope_at(rfs + P + k, cs, cs + kMaxHalfTaps + 1, P);
+    const size_t o = ((size_t)f * a.L + line) * S + k;
+    if (a.ref_fixed) {
+      const float y = env > 0.f ? fminf(fmaxf(fmaf(a.log_k1, log2f(env), a.log_k0), 0.f), 1.f) : 0.f;
+      if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[o] = (uint8_t)floorf(255.f * y + 0.5f);
+      else ((float*)a.y_out)[o] = y;
+    } else {
+      a.env_out[o] = env;
+      m = fmaxf(m, env);
+    }
+  }
+  if (!a.ref_fixed) {
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&smax, __float_as_uint(m));
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&a.frame_max[f], smax);
+  }
 }
 
 // y = 1 + (20 log10 2 / DR) (log2 env - log2 ref), clamped to [0,1]; env = 0
@@ -77,7 +99,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
 
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st) {
   const int P = (a.fir_taps - 1) / 2;
-  size_t smem = ((sizeof(float2) * a.fir_taps + 15) & ~size_t(15)) + sizeof(float) * (a.S + 2 * P) + 64;
+  size_t smem = sizeof(float) * (2 * (kMaxHalfTaps + 1) + a.S + 2 * P);
   cudaError_t e = cudaFuncSetAttribute(envlog_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.L, a.F);

@@ -77,6 +77,7 @@ struct supra_bf {
   std::vector<ScAxis> h_ax, h_az;
   std::vector<ScRow> h_rows;
   std::vector<ScEntry> h_ent;
+  std::vector<float> fir_c, fir_s;
   int64_t info[8] = {0};
 };
 
@@ -309,6 +310,12 @@ supra_status build_das_tables(supra_bf* h) {
     double hj = hd[j + P] / sum;
     fir[j + P] = make_float2((float)(hj * std::cos(om * j)), (float)(hj * std::sin(om * j)));
   }
+  h->fir_c.assign(kMaxHalfTaps + 1, 0.f);
+  h->fir_s.assign(kMaxHalfTaps + 1, 0.f);
+  for (int j = 0; j <= P; j++) {
+    h->fir_c[j] = fir[j + P].x;
+    h->fir_s[j] = fir[j + P].y;
+  }
   cudaError_t e;
   if ((e = upload(&h->d_line_group, line_group)) != cudaSuccess ||
       (e = upload(&h->d_entries, flat)) != cudaSuccess || (e = upload(&h->d_ntile, ntile)) != cudaSuccess ||
@@ -459,6 +466,37 @@ supra_status build_sc_tables(supra_bf* h) {
   return SUPRA_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// raw [F][E][C][S] int16 viewed as u32 sample pairs {S/2, C, E, F}; box
+// {kWin/2, 1, 1, fb}; out-of-bounds elements read as zero.
+bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, int fb) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)S / 2, (cuuint64_t)C, (cuuint64_t)E, (cuuint64_t)F};
+  cuuint64_t strides[3] = {(cuuint64_t)S * 2, (cuuint64_t)C * S * 2, (cuuint64_t)E * C * S * 2};
+  cuuint32_t box[4] = {(cuuint32_t)(kWin / 2), 1, 1, (cuuint32_t)fb};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(raw), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool is_device_ptr(const void* p, int dev) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -582,6 +620,10 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
   a.do_epilogue = line_img != nullptr;
   a.fir = h->d_fir;
   a.fir_taps = c.fir_taps;
+  for (int j = 0; j <= kMaxHalfTaps; j++) {
+    a.fir_c[j] = h->fir_c[j];
+    a.fir_s[j] = h->fir_s[j];
+  }
   fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
   a.y_type = c.line_output_type;
   if (line_img) {
@@ -594,7 +636,11 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
-  supra_status s = check_launch(launch_das(a, h->frames_per_cta, h->das_smem, st), "das kernel");
+  const int fb = das_frames_per_cta(h->frames_per_cta, frames);
+  CUtensorMap tm;
+  if (!make_raw_map(&tm, raw, frames, h->E, h->C, h->S, fb))
+    return fail(SUPRA_E_CUDA, "cuTensorMapEncodeTiled failed for the raw buffer");
+  supra_status s = check_launch(launch_das(tm, a, fb, st), "das kernel");
   if (s != SUPRA_OK || !line_img || a.ref_fixed) return s;
   FinalizeArgs fa{};
   fa.env = a.env_out;

@@ -2,6 +2,7 @@
 // kernels (das.cu, epilogue.cu, scanconv.cu).  Not part of the public ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "supra_bf.h"
@@ -19,6 +20,10 @@ constexpr int kWin = kTileK + 24;
 constexpr int kStages = 4;
 // Producer lanes == bulk copies per stage (entries-per-stage x frames-per-CTA).
 constexpr int kCopiesPerStage = 32;
+// FIR half-length limit (fir_taps <= 2*kMaxHalfTaps + 1 = 129).
+constexpr int kMaxHalfTaps = 64;
+// Rolling RF ring of the fused epilogue: 4 depth tiles.
+constexpr int kRing = 4 * kTileK;
 
 // One receive-aperture entry of a line group (lines sharing an origin),
 // sorted by k_enter.  Lengths in "sample units" (mm * fs / (1000 c)), in
@@ -50,6 +55,12 @@ struct DasArgs {
   int do_epilogue;             // 1: FIR + envelope (+ log) epilogue
   const float2* fir;           // [T] complex taps g_j = h_j e^{+i w j}, j = -P..P
   int fir_taps;
+  // the same taps split by symmetry (reading #18): c_j = Re g_j (even),
+  // s_j = Im g_{-j} = -Im g_j ... stored for j = 0..P as c[j] = Re g_j,
+  // s[j] = Im g_j; passed by value so the unrolled FIR reads them from the
+  // constant bank (uniform-register operands of FFMA2).
+  float fir_c[kMaxHalfTaps + 1];
+  float fir_s[kMaxHalfTaps + 1];
   int ref_fixed;               // 1: y written directly; 0: env written + frame max
   float log_k1, log_k0;        // y = k1 log2(env) + k0 (fixed reference)
   float* env_out;              // [F][L][S] f32 (frame-max mode)
@@ -117,7 +128,10 @@ struct ScArgs {
 };
 
 // Launchers (return cudaGetLastError()).
-cudaError_t launch_das(const DasArgs& a, int frames_per_cta, size_t smem_bytes, cudaStream_t st);
+// raw is addressed through a 4-D tensor map {S/2 sample pairs (u32), C, E, F}
+// with box {kWin/2, 1, 1, fb}; fb = das_frames_per_cta(configured, F).
+cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, int fb, cudaStream_t st);
+int das_frames_per_cta(int fb, int F);
 size_t das_smem_bytes(int frames_per_cta, int S, int fir_taps);
 int das_max_frames_per_cta(int S, int fir_taps, int F);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
