@@ -2,27 +2,29 @@
 // IQ-envelope / log-compression epilogue (
 // S:133).
 //
-// One CTA = one scanline x FB frames, all depth tiles of the line.
-// Warp-specialised, 9 warps:
-//   warp 8 (producer): per stage, 32 lanes each bulk-copy (cp.async.bulk ->
-//     SASS UBLKCP, the 1-D TMA) one (aperture entry, frame) window of int16
-//     samples -- only the samples the tile's delays reference -- into a
-//     4-stage shared-memory ring; completion via mbarrier tx-counts.  The
-//     producer also writes a per-stage entry record {|q|^2/2, d.q, pi*cu,
-//     k_enter} and the window start, so consumers do no dot products.
-//   warps 0-7 (consumers): one output depth sample k per thread per 256-
-//     sample tile; per aperture entry: the closed-form split delay
-//     tau = k + delta, delta = |q + h d| - h (h = k/2, sample units) with one
-//     MUFU.RSQ and a Newton correction (reading #30), magic-number floor,
-//     Hann weight (MUFU.COS), then for every frame pair the int16 -> f32
+// One CTA = one scanline x FB frames.  The loop runs over the line's receive
+// aperture entries (channels, pre-sorted by aperture entry depth k_enter in
+// binary64, reading #6); every consumer thread keeps the RF of its NT output
+// samples k = kt + 256 m for all FB frames in registers.  Warp-specialised:
+//   warp 8 (producer): per entry ONE 5-D TMA (cp.async.bulk.tensor -> SASS
+//     UTMALDG) fetches the entry's whole referenced trace [ws, S) for the FB
+//     frames into a 3-stage shared-memory ring -- each referenced sample is
+//     read from HBM once, the start is 32-sample aligned, samples < 0 or
+//     >= S come back as zeros (the TMA out-of-bounds fill = the zero
+//     padding of reading #10).  It also publishes the entry record
+//     {|q|^2/2, d.q, pi cu, k_enter} so consumers do no dot products.
+//   warps 0-7 (consumers): per entry and output tile, the closed-form split
+//     delay tau = k + delta, delta = |q + h d| - h (h = k/2 in sample units)
+//     with one MUFU.RSQ + Newton correction (reading #30), magic-number
+//     floor, Hann weight (MUFU.COS), then for each frame pair the int16->f32
 //     magic conversion, linear interpolation and accumulation in packed
 //     f32x2 (FADD2/FFMA2): geometry is amortised over the FB frames.
-// Aperture entries are pre-sorted by k_enter (binary64, reading #6): the
-// members of a tile are a prefix of the list, per-lane membership is one
-// integer compare.  RF lines go to a 4-tile ring in shared memory; after
-// each tile the consumers run the 65-tap complex FIR of the previous tile
-// (symmetric form, taps in the constant bank), |.|, and either 20 log10
-// against a fixed reference or env + per-frame max (frame-max reference).
+// After the last entry RF = sum / N (N from a binary64-derived count table)
+// is written to shared memory (reusing the trace ring) in a padded,
+// bank-conflict-free layout and the epilogue runs the 65-tap complex FIR as
+// a sliding window (4 outputs x 4 frames per thread, taps in the constant
+// bank), |.|, then 20 log10 against a fixed reference, or env + per-frame
+// max for the frame-max reference (finalised by finalize_kernel).
 #include "internal.h"
 
 namespace supra {
@@ -60,24 +62,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+// 5-D TMA tile load: box {16 pairs, rows, 1 channel, 1 event, FB frames}.
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            int c4, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// 4-D TMA tile load (SASS UTMALDG): box {kWin/2 sample pairs, 1 channel,
-// 1 event, FB frames} at coordinates (c0, c1, c2, c3); out-of-range
-// coordinates (samples < 0 or >= S, frames >= F) are zero-filled by the TMA
-// unit, which is exactly the zero padding of reading #10.
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -87,6 +78,12 @@ __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -116,133 +113,215 @@ __device__ __forceinline__ float split_delay(float Ah, float B, float h, float h
 // int16 -> float via the 2^23 + 2^15 magic: bits (u ^ 0x4B008000) of the
 // zero-extended 16-bit value u are the float 2^23 + 2^15 + v.
 __device__ __forceinline__ float magic16(uint32_t u) { return __int_as_float((int)(u ^ 0x4B008000u)); }
-constexpr float kMagic16 = 8421376.0f;  // 2^23 + 2^15
+constexpr float kMagic16 = 8421376.0f;      // 2^23 + 2^15
 constexpr float kFloorMagic = 12582912.0f;  // 1.5 * 2^23
 constexpr int kFloorMagicBits = 0x4B400000;
+constexpr int kHalo = 64;                   // FIR halo (>= kMaxHalfTaps), each side
 
-__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
+
+// Trace stage: FB frames x rows x 32 samples (int16), 128-byte aligned.
+__host__ __device__ inline size_t stage_bytes(int FB, int rows) {
+  return align128((size_t)FB * rows * kRowSamples * 2);
+}
+// FIR line buffer: ngroups x padded(S + 2 halo + 4) float4 (4 frames), with
+// a 16-byte pad after every 4 samples (conflict-free sliding LDS.128).
+__host__ __device__ inline int fir_pad(int kp) { return kp + (kp >> 2); }
+__host__ __device__ inline int fir_span(int S) { return fir_pad(S + 2 * kHalo + 4); }
+__host__ __device__ inline size_t fir_bytes(int FB, int S) {
+  return align128((size_t)((FB + 3) / 4) * fir_span(S) * 16);
+}
 
 struct SmemLayout {
-  int16_t* stage;  // [kStages][EC][block]: FB x kWin int16 per entry
-  float4* rec;     // [kStages][32] {Ah, B, pi*cu, k_enter bits}
-  int* ws;         // [kStages][32]
-  uint64_t* full;  // [kStages]
-  uint64_t* empty; // [kStages]
-  float* ring;     // [kRing][FB]  (frame fastest)
-  unsigned* smax;  // [8]
+  int16_t* stage;   // [kStages][stage_bytes]
+  float4* rec;      // [kStages] {Ah, B, pi*cu, k_enter bits}
+  int* ws;          // [kStages]
+  uint64_t* full;   // [kStages]
+  uint64_t* empty;  // [kStages]
+  unsigned* smax;   // [8]
+  float4* line;     // FIR buffer, aliases the stage ring after the DAS loop
 };
 
-// One staged entry block: FB frames x kWin samples, 128-byte aligned (TMA).
-__host__ __device__ constexpr int block_bytes(int FB) { return (FB * kWin * 2 + 127) & ~127; }
-
-__host__ __device__ inline size_t layout_bytes(int FB, size_t* off) {
+__host__ __device__ inline size_t layout_bytes(int FB, int S, size_t* off) {
+  const int rows = das_rows(S);
+  const size_t ring = (size_t)kStages * stage_bytes(FB, rows);
+  const size_t fb = fir_bytes(FB, S);
   size_t o = 0;
-  off[0] = o; o = align16(o + (size_t)kStages * (kCopiesPerStage / FB) * block_bytes(FB));
-  off[1] = o; o = align16(o + sizeof(float4) * kStages * kCopiesPerStage);
-  off[2] = o; o = align16(o + sizeof(int) * kStages * kCopiesPerStage);
-  off[3] = o; o = align16(o + sizeof(uint64_t) * kStages);
-  off[4] = o; o = align16(o + sizeof(uint64_t) * kStages);
-  off[5] = o; o = align16(o + sizeof(float) * (size_t)kRing * FB);
-  off[6] = o; o = align16(o + sizeof(unsigned) * 8);
+  off[0] = o; o = align128(o + (ring > fb ? ring : fb));
+  off[1] = o; o = align128(o + sizeof(float4) * kStages);
+  off[2] = o; o = align128(o + sizeof(int) * kStages);
+  off[3] = o; o = align128(o + sizeof(uint64_t) * kStages);
+  off[4] = o; o = align128(o + sizeof(uint64_t) * kStages);
+  off[5] = o; o = align128(o + sizeof(unsigned) * 8);
   return o;
 }
 
-__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB) {
-  size_t off[7];
-  layout_bytes(FB, off);
+__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int S) {
+  size_t off[6];
+  layout_bytes(FB, S, off);
   SmemLayout L;
   L.stage = (int16_t*)(base + off[0]);
+  L.line = (float4*)(base + off[0]);
   L.rec = (float4*)(base + off[1]);
   L.ws = (int*)(base + off[2]);
   L.full = (uint64_t*)(base + off[3]);
   L.empty = (uint64_t*)(base + off[4]);
-  L.ring = (float*)(base + off[5]);
-  L.smax = (unsigned*)(base + off[6]);
+  L.smax = (unsigned*)(base + off[5]);
   return L;
 }
 
 // ---------------------------------------------------------------------------
-// Envelope + log of one output sample k for all FB frames from the RF ring.
+// Epilogue: envelope of 4 consecutive outputs k0..k0+3 for the 4 frames of
+// one frame group (sliding window over the padded line buffer; x(k) = 0
+// outside [0, S)), then log compression or env + running max.
 // b[k] = c0 x[k] + sum_{j>=1} c_j (x[k-j] + x[k+j]) + i s_j (x[k-j] - x[k+j])
-// (reading #18; symmetric h), env = 2|b|.
+// (reading #18: g_j = h_j e^{+i w j}, h symmetric), env = 2 |b|.
 template <int FB>
-__device__ __forceinline__ void fir_output(const DasArgs& a, const float* ring, int k, int line, int f0,
-                                           float* bmax) {
+__device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int k0, int line, int fg0,
+                                          float* bmax) {
   const int P = (a.fir_taps - 1) / 2;
-  const int p0 = k & (kRing - 1);
-  float env[FB];
-  if constexpr (FB == 1) {
-    float re = a.fir_c[0] * ring[p0], im = 0.f;
+  auto X = [&](int k) { return lineg[fir_pad(k + kHalo)]; };
+  float4 Lw[4], Rw[4];
 #pragma unroll
-    for (int j = 1; j <= kMaxHalfTaps; j++) {
-      if (j > P) break;
-      const float xm = ring[(k - j) & (kRing - 1)];
-      const float xp = ring[(k + j) & (kRing - 1)];
-      re = fmaf(a.fir_c[j], xm + xp, re);
-      im = fmaf(a.fir_s[j], xm - xp, im);
-    }
-    env[0] = 2.f * sqrtf(fmaf(re, re, im * im));
-  } else {
-    constexpr int NP = FB / 2;
-    float2 re[NP], im[NP];
-    const float2* r2 = reinterpret_cast<const float2*>(ring);
+  for (int o = 0; o < 4; o++) Lw[o] = Rw[o] = X(k0 + o);
+  float2 re[4][2], im[4][2];
+  const float c0 = a.fir_c[0];
 #pragma unroll
-    for (int q = 0; q < NP; q++) {
-      re[q] = __fmul2_rn(make_float2(a.fir_c[0], a.fir_c[0]), r2[p0 * NP + q]);
-      im[q] = make_float2(0.f, 0.f);
-    }
+  for (int o = 0; o < 4; o++) {
+    re[o][0] = __fmul2_rn(make_float2(c0, c0), make_float2(Lw[o].x, Lw[o].y));
+    re[o][1] = __fmul2_rn(make_float2(c0, c0), make_float2(Lw[o].z, Lw[o].w));
+    im[o][0] = im[o][1] = make_float2(0.f, 0.f);
+  }
 #pragma unroll
-    for (int j = 1; j <= kMaxHalfTaps; j++) {
-      if (j > P) break;
-      const int pm = (k - j) & (kRing - 1), pp = (k + j) & (kRing - 1);
+  for (int j = 1; j <= kMaxHalfTaps; j++) {
+    if (j > P) break;
+    // shift: Lw[o] = x[k0 + o - j], Rw[o] = x[k0 + o + j]
+    Lw[3] = Lw[2]; Lw[2] = Lw[1]; Lw[1] = Lw[0]; Lw[0] = X(k0 - j);
+    Rw[0] = Rw[1]; Rw[1] = Rw[2]; Rw[2] = Rw[3]; Rw[3] = X(k0 + 3 + j);
+    const float2 cj = make_float2(a.fir_c[j], a.fir_c[j]), sj = make_float2(a.fir_s[j], a.fir_s[j]);
 #pragma unroll
-      for (int q = 0; q < NP; q++) {
-        const float2 xm = r2[pm * NP + q], xp = r2[pp * NP + q];
-        re[q] = __ffma2_rn(make_float2(a.fir_c[j], a.fir_c[j]), __fadd2_rn(xm, xp), re[q]);
-        im[q] = __ffma2_rn(make_float2(a.fir_s[j], a.fir_s[j]), sub2(xm, xp), im[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NP; q++) {
-      const float2 e2 = __ffma2_rn(re[q], re[q], __fmul2_rn(im[q], im[q]));
-      env[2 * q] = 2.f * sqrtf(e2.x);
-      env[2 * q + 1] = 2.f * sqrtf(e2.y);
+    for (int o = 0; o < 4; o++) {
+      const float2 l0 = make_float2(Lw[o].x, Lw[o].y), l1 = make_float2(Lw[o].z, Lw[o].w);
+      const float2 r0 = make_float2(Rw[o].x, Rw[o].y), r1 = make_float2(Rw[o].z, Rw[o].w);
+      re[o][0] = __ffma2_rn(cj, __fadd2_rn(l0, r0), re[o][0]);
+      re[o][1] = __ffma2_rn(cj, __fadd2_rn(l1, r1), re[o][1]);
+      im[o][0] = __ffma2_rn(sj, sub2(l0, r0), im[o][0]);
+      im[o][1] = __ffma2_rn(sj, sub2(l1, r1), im[o][1]);
     }
   }
-  if (k >= a.S) return;
 #pragma unroll
-  for (int b = 0; b < FB; b++) {
-    const int f = f0 + b;
-    if (f >= a.F) break;
-    const size_t o = ((size_t)f * a.L + line) * a.S + k;
-    if (a.ref_fixed) {
-      const float e = env[b];
-      const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, log2f(e), a.log_k0), 0.f), 1.f) : 0.f;
-      if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[o] = (uint8_t)floorf(255.f * y + 0.5f);
-      else ((float*)a.y_out)[o] = y;
-    } else {
-      a.env_out[o] = env[b];
-      bmax[b] = fmaxf(bmax[b], env[b]);
+  for (int o = 0; o < 4; o++) {
+    const int k = k0 + o;
+    if (k >= a.S) break;
+    const float2 e0 = __ffma2_rn(re[o][0], re[o][0], __fmul2_rn(im[o][0], im[o][0]));
+    const float2 e1 = __ffma2_rn(re[o][1], re[o][1], __fmul2_rn(im[o][1], im[o][1]));
+    const float env[4] = {2.f * sqrtf(e0.x), 2.f * sqrtf(e0.y), 2.f * sqrtf(e1.x), 2.f * sqrtf(e1.y)};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int f = fg0 + q;
+      if (q >= FB || f >= a.F) break;
+      const size_t out = ((size_t)f * a.L + line) * a.S + k;
+      if (a.ref_fixed) {
+        const float e = env[q];
+        const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, log2f(e), a.log_k0), 0.f), 1.f) : 0.f;
+        if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[out] = (uint8_t)floorf(255.f * y + 0.5f);
+        else ((float*)a.y_out)[out] = y;
+      } else {
+        a.env_out[out] = env[q];
+        bmax[q] = fmaxf(bmax[q], env[q]);
+      }
     }
   }
 }
 
 }  // namespace
 
-template <int FB, bool T0>
-__global__ void __launch_bounds__(288, 2) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
+// Accumulators of one thread: NT output samples x FB frames.
+template <int FB, int NT>
+struct Acc {
+  float s[FB == 1 ? NT : 1];
+  float2 p[FB >= 2 ? NT : 1][FB >= 2 ? FB / 2 : 1];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int m = 0; m < NT; m++) {
+      if constexpr (FB == 1) {
+        s[m] = 0.f;
+      } else {
+#pragma unroll
+        for (int q = 0; q < FB / 2; q++) p[m][q] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+};
+
+// Specialisation granularity of the first active tile (code size).
+__host__ __device__ constexpr int tile_gran(int NT) { return NT <= 8 ? 1 : 2; }
+
+// One aperture entry, output tiles M0 .. NT-1 (straight-line).
+template <int FB, int NT, int M0, bool T0>
+__device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, int kenter, int wsm,
+                                            const unsigned short* st, int kt, float ktf, int S,
+                                            Acc<FB, NT>& acc) {
+  constexpr int FR = (NT * 8 + 2) * kRowSamples;
+#pragma unroll
+  for (int m = M0; m < NT; m++) {
+    const int k = m * kTileK + kt;
+    const bool mem = (k >= kenter) && (k < S);
+    const float kf = ktf + (float)(m * kTileK);
+    const float h = 0.5f * kf;
+    const float h2 = (m == 0 && kt == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
+    float delta = split_delay(r.x, r.y, h, h2);
+    if (T0) delta += a.t0fs;
+    const float tf = __fadd_rd(delta, kFloorMagic);
+    int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - kt)
+    const float fr = delta - (tf - kFloorMagic);
+    idx = mem ? idx : 0;
+    float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
+    w = mem ? w : 0.f;
+    const float wf = w * fr;
+    const unsigned short* px = st + idx;
+    if constexpr (FB == 1) {
+      const float m0 = magic16(px[0]), m1 = magic16(px[1]);
+      acc.s[m] = fmaf(w, m0 - kMagic16, acc.s[m]);
+      acc.s[m] = fmaf(wf, m1 - m0, acc.s[m]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < FB / 2; q++) {
+        const float2 m0 = make_float2(magic16(px[(2 * q) * FR]), magic16(px[(2 * q + 1) * FR]));
+        const float2 m1 = make_float2(magic16(px[(2 * q) * FR + 1]), magic16(px[(2 * q + 1) * FR + 1]));
+        acc.p[m][q] = __ffma2_rn(make_float2(w, w), __fadd2_rn(m0, make_float2(-kMagic16, -kMagic16)),
+                                 acc.p[m][q]);
+        acc.p[m][q] = __ffma2_rn(make_float2(wf, wf), sub2(m1, m0), acc.p[m][q]);
+      }
+    }
+  }
+}
+
+template <int FB, int NT, bool T0, int G = 0>
+__device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const float4& r, int kenter, int wsm,
+                                               const unsigned short* st, int kt, float ktf, int S,
+                                               Acc<FB, NT>& acc) {
+  constexpr int M0 = G * tile_gran(NT);
+  if constexpr (M0 < NT) {
+    if (g == G) entry_tiles<FB, NT, M0, T0>(a, r, kenter, wsm, st, kt, ktf, S, acc);
+    else dispatch_tiles<FB, NT, T0, G + 1>(g, a, r, kenter, wsm, st, kt, ktf, S, acc);
+  }
+}
+
+template <int FB, int NT, bool T0>
+__global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const DasArgs a) {
-  constexpr int EC = kCopiesPerStage / FB;  // aperture entries per stage
-  constexpr int BLK = block_bytes(FB) / 2;  // int16 elements per entry block
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int S = a.S;
-  SmemLayout sm = carve(smem_raw, FB);
+  constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
+  const size_t SB = stage_bytes(FB, NT * 8 + 2);
+  SmemLayout sm = carve(smem_raw, FB, S);
   const int line = blockIdx.x;
   const int f0 = blockIdx.y * FB;
   const int g = a.line_group[line];
   const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
-  const int* __restrict__ ntile = a.ntile + (size_t)g * a.ntiles;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nent = a.nentries[g];
+  const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; i++) {
@@ -252,199 +331,171 @@ __global__ void __launch_bounds__(288, 2) das_fused_kernel(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < 8) sm.smax[threadIdx.x] = 0u;
-  // ring slot 3 holds "tile -1": zeros for the FIR's left edge (k < 0)
-  for (int i = threadIdx.x; i < kTileK * FB; i += blockDim.x) sm.ring[3 * kTileK * FB + i] = 0.f;
   __syncthreads();
 
-  if (warp == 8) {
-    // ------------------------------ producer ------------------------------
-    // lane jl < EC owns entry c*EC + jl of each stage: it computes the
-    // window, writes the entry record and issues one 4-D TMA covering the
-    // window for all FB frames.
-    const int ev = a.line_event[line];
-    const float4 dir = a.line_dir[line];
-    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-    int s = 0;
-    for (int t = 0; t < a.ntiles; t++) {
-      const int nt = ntile[t];
-      const int nch = (nt + EC - 1) / EC;
-      const int k0 = t * kTileK, k1 = min(k0 + kTileK, S) - 1;
-      for (int c = 0; c < nch; c++, s++) {
-        const int buf = s % kStages;
-        if (s >= kStages) mbar_wait(&sm.empty[buf], ((s / kStages) - 1) & 1);
-        const int j = c * EC + lane;
-        const bool valid = lane < EC && j < nt;
-        int ws = 0, kenter = 0x7fffffff;
-        if (lane < EC) {
-          const DasEntry e = ents[j];
-          const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
-          const float Ah = 0.5f * e.A;
-          if (valid) {
-            kenter = e.kenter;
-            const int kb = max(k0, e.kenter);
-            const float hb = 0.5f * (float)kb;
-            const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
-            // window [ws, ws + kWin): ws <= floor(tau(kb)) - 2, 8-aligned; the
-            // end floor(tau(k1)) + 3 <= ws + kWin because d tau / dk <= 1.
-            ws = ((int)floorf(tb) - 2) & ~7;
-          }
-          sm.rec[buf * kCopiesPerStage + lane] = make_float4(Ah, B, 3.14159265358979f * e.cu,
-                                                             __int_as_float(kenter));
-          sm.ws[buf * kCopiesPerStage + lane] = ws;
-        }
-        const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, valid));
-        if (lane == 0) mbar_arrive_tx(&sm.full[buf], nvalid * (unsigned)(FB * kWin * 2));
-        __syncwarp();
-        if (valid) {
-          int16_t* dst = sm.stage + ((size_t)buf * EC + lane) * BLK;
-          tma_load_4d(dst, &tmap, ws >> 1, ents[j].elem, ev, f0, &sm.full[buf]);
-        }
-      }
-    }
-  } else {
+  // Producer role (thread 0, inline): issue the TMA of entry jj into ring
+  // slot jj % kStages once every warp has released that slot.
+  const int ev = a.line_event[line];
+  const float4 dir = a.line_dir[line];
+  auto produce = [&](int jj) {
+    const int buf = jj % kStages;
+    if (jj >= kStages) mbar_wait(&sm.empty[buf], ((jj / kStages) - 1) & 1);
+    const DasEntry e = ents[jj];
+    const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
+    const float Ah = 0.5f * e.A;
+    const int kb = e.kenter;
+    const float hb = 0.5f * (float)kb;
+    const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
+    // window [ws, ws + rows*32), rows = S/32 + 2, ws <= floor(tau(k_enter)) - 2
+    // and 32-aligned: d tau/dk in [0, 1] gives i0(k) + 1 <= ws + S + 34
+    // for every member k < S, inside the window; reads past the record
+    // (>= S) or before it (< 0) come back as TMA zeros.
+    const int ws = ((int)floorf(tb) - 2) & ~(kRowSamples - 1);
+    sm.rec[buf] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(kb));
+    sm.ws[buf] = ws;
+    mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
+    tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, ws / kRowSamples, e.elem, ev, f0,
+                &sm.full[buf]);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    for (int jj = 0; jj < kStages - 1 && jj < nent; jj++) produce(jj);
+  }
+
+  {
     // ------------------------------ consumers -----------------------------
-    const int kt = warp * 32 + lane;
-    float bmax[FB];
+    const int kt = threadIdx.x;
+    const float ktf = (float)kt;
+    Acc<FB, NT> acc;
+    acc.zero();
+    for (int j = 0; j < nent; j++) {
+      if (threadIdx.x == 0 && j + kStages - 1 < nent) produce(j + kStages - 1);
+      const int buf = j % kStages;
+      mbar_wait(&sm.full[buf], (j / kStages) & 1);
+      const float4 r = sm.rec[buf];
+      const int kenter = __float_as_int(r.w);
+      const int wsm = sm.ws[buf] + kFloorMagicBits - kt;
+      const unsigned short* st = (const unsigned short*)((const unsigned char*)sm.stage + buf * SB);
+      // straight-line code for the tiles at or after the entry's first
+      // active tile (no per-tile branches: the chains of consecutive tiles
+      // interleave)
+      dispatch_tiles<FB, NT, T0>(min(kenter / kTileK, NT - 1) / tile_gran(NT), a, r, kenter, wsm, st, kt, ktf, S,
+                                 acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[buf]);
+    }
+    // ---- RF = sum / N (reading #7; 0 when N = 0) ----
+    const uint16_t* ncount = a.ncount + (size_t)g * S;
+    __syncthreads();  // every warp is done with the trace ring (aliased below)
+    const int span = fir_span(S);
 #pragma unroll
-    for (int b = 0; b < FB; b++) bmax[b] = 0.f;
-    int s = 0;
-    for (int t = 0; t < a.ntiles; t++) {
-      const int k = t * kTileK + kt;
-      const bool kval = k < S;
-      const float kf = (float)k, h = 0.5f * kf;
-      const float h2 = k > 0 ? h * h : 1e-20f;   // r2 > 0 even at k = 0, q = 0
-      const float inv_k = k > 0 ? 1.0f / kf : 0.f;
-      const int kmw = k - kFloorMagicBits;
-      float acc1 = 0.f;
-      float2 acc2[FB / 2 > 0 ? FB / 2 : 1];
-#pragma unroll
-      for (int q = 0; q < FB / 2; q++) acc2[q] = make_float2(0.f, 0.f);
-      int cnt = 0;
-      const int nt = ntile[t];
-      const int nch = (nt + EC - 1) / EC;
-      for (int c = 0; c < nch; c++, s++) {
-        const int buf = s % kStages;
-        mbar_wait(&sm.full[buf], (s / kStages) & 1);
-        const float4* rec = sm.rec + buf * kCopiesPerStage;
-        const int* wsb = sm.ws + buf * kCopiesPerStage;
-        const unsigned short* st = (const unsigned short*)(sm.stage + (size_t)buf * EC * BLK);
-#pragma unroll
-        for (int jl = 0; jl < EC; jl++) {
-          const float4 r = rec[jl];
-          const int ws = wsb[jl];
-          const bool mem = kval && (k >= __float_as_int(r.w));
-          float delta = split_delay(r.x, r.y, h, h2);
-          if (T0) delta += a.t0fs;
-          const float tf = __fadd_rd(delta, kFloorMagic);
-          int idx = __float_as_int(tf) + kmw - ws;
-          const float fr = delta - (tf - kFloorMagic);
-          idx = mem ? idx : 0;
-          float w = fmaf(__cosf(r.z * inv_k), a.win_b, a.win_a);
-          w = mem ? w : 0.f;
-          const float wf = w * fr;
-          cnt += mem ? 1 : 0;
-          const unsigned short* px = st + jl * BLK + idx;
-          if constexpr (FB == 1) {
-            const float m0 = magic16(px[0]), m1 = magic16(px[1]);
-            acc1 = fmaf(w, m0 - kMagic16, acc1);
-            acc1 = fmaf(wf, m1 - m0, acc1);
-          } else {
-#pragma unroll
-            for (int q = 0; q < FB / 2; q++) {
-              const float2 m0 = make_float2(magic16(px[(2 * q) * kWin]), magic16(px[(2 * q + 1) * kWin]));
-              const float2 m1 =
-                  make_float2(magic16(px[(2 * q) * kWin + 1]), magic16(px[(2 * q + 1) * kWin + 1]));
-              acc2[q] = __ffma2_rn(make_float2(w, w), __fadd2_rn(m0, make_float2(-kMagic16, -kMagic16)),
-                                   acc2[q]);
-              acc2[q] = __ffma2_rn(make_float2(wf, wf), sub2(m1, m0), acc2[q]);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[buf]);
-      }
-      // ---- tile done: RF = sum / N  (reading #7; 0 when N = 0) ----
-      const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (cnt > 0 ? 1.f / (float)cnt : 0.f);
+    for (int m = 0; m < NT; m++) {
+      if (m * kTileK >= S) break;
+      const int k = m * kTileK + kt;
+      if (k >= S) break;
+      const int n = (int)ncount[k];
+      const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
       float v[FB];
       if constexpr (FB == 1) {
-        v[0] = kval ? acc1 * inv : 0.f;
+        v[0] = acc.s[m] * inv;
       } else {
 #pragma unroll
         for (int q = 0; q < FB / 2; q++) {
-          v[2 * q] = kval ? acc2[q].x * inv : 0.f;
-          v[2 * q + 1] = kval ? acc2[q].y * inv : 0.f;
+          v[2 * q] = acc.p[m][q].x * inv;
+          v[2 * q + 1] = acc.p[m][q].y * inv;
         }
       }
-      if (a.rf && kval) {
+      if (a.rf) {
 #pragma unroll
         for (int b = 0; b < FB; b++)
           if (f0 + b < a.F) a.rf[((size_t)(f0 + b) * a.L + line) * S + k] = v[b];
       }
       if (a.do_epilogue) {
-        float* slot = sm.ring + (size_t)(k & (kRing - 1)) * FB;
+        const int pk = fir_pad(k + kHalo);
 #pragma unroll
-        for (int b = 0; b < FB; b++) slot[b] = v[b];
-        consumer_sync();
-        if (t >= 1) fir_output<FB>(a, sm.ring, k - kTileK, line, f0, bmax);
-      }
-    }
-    if (a.do_epilogue) {
-      // zero the slot after the last tile (the FIR's right edge, k >= S)
-      const int kz = a.ntiles * kTileK + kt;
-      float* slot = sm.ring + (size_t)(kz & (kRing - 1)) * FB;
-#pragma unroll
-      for (int b = 0; b < FB; b++) slot[b] = 0.f;
-      consumer_sync();
-      fir_output<FB>(a, sm.ring, (a.ntiles - 1) * kTileK + kt, line, f0, bmax);
-      if (!a.ref_fixed) {
-#pragma unroll
-        for (int b = 0; b < FB; b++) {
-          float m = bmax[b];
-          for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-          if (lane == 0) atomicMax(&sm.smax[b], __float_as_uint(m));
+        for (int q4 = 0; q4 < (FB + 3) / 4; q4++) {
+          float4 x;
+          x.x = v[4 * q4];
+          x.y = (4 * q4 + 1 < FB) ? v[(4 * q4 + 1) % FB] : 0.f;
+          x.z = (4 * q4 + 2 < FB) ? v[(4 * q4 + 2) % FB] : 0.f;
+          x.w = (4 * q4 + 3 < FB) ? v[(4 * q4 + 3) % FB] : 0.f;
+          sm.line[(size_t)q4 * span + pk] = x;
         }
-        consumer_sync();
-        if (kt < FB && f0 + kt < a.F) atomicMax(&a.frame_max[f0 + kt], sm.smax[kt]);
       }
     }
   }
+  if (!a.do_epilogue) return;
+  const int ng = (FB + 3) / 4, span = fir_span(S);
+  // zero halos: padded positions of k' in [0, kHalo) and [kHalo + S, S + 2 kHalo + 4)
+  for (int i = threadIdx.x; i < ng * (2 * kHalo + 4); i += blockDim.x) {
+    const int q4 = i / (2 * kHalo + 4), r = i - q4 * (2 * kHalo + 4);
+    const int kp = r < kHalo ? r : S + r;
+    sm.line[(size_t)q4 * span + fir_pad(kp)] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  // ---- epilogue: work items = (frame group, 4 consecutive outputs) ----
+  const int nblk = (S + 3) / 4;
+  float bmax[4] = {0.f, 0.f, 0.f, 0.f};
+  int curg = -1;
+  for (int it = threadIdx.x; it < ng * nblk; it += blockDim.x) {
+    const int q4 = it / nblk, blk = it - q4 * nblk;
+    if (q4 != curg) {
+      if (curg >= 0 && !a.ref_fixed)
+        for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
+      curg = q4;
+      bmax[0] = bmax[1] = bmax[2] = bmax[3] = 0.f;
+    }
+    fir_block<FB>(a, sm.line + (size_t)q4 * span, 4 * blk, line, f0 + 4 * q4, bmax);
+  }
+  if (!a.ref_fixed) {
+    if (curg >= 0)
+      for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
+    __syncthreads();
+    if (threadIdx.x < FB && f0 + (int)threadIdx.x < a.F)
+      atomicMax(&a.frame_max[f0 + threadIdx.x], sm.smax[threadIdx.x]);
+  }
 }
 
-size_t das_smem_bytes(int FB, int, int) {
-  size_t off[7];
-  return layout_bytes(FB, off);
+size_t das_smem_bytes(int FB, int S, int) {
+  size_t off[6];
+  return layout_bytes(FB, S, off);
 }
 
-int das_max_frames_per_cta(int, int, int F) {
-  for (int fb = 8; fb > 1; fb >>= 1)
-    if (fb <= F) return fb;
-  return 1;
+// Frames per CTA: registers hold NT x FB accumulators (<= 64), the smem
+// footprint must allow 2 CTAs per SM, and never more frames than the call.
+int das_frames_per_cta(int fb_max, int S, int F) {
+  const int nt = das_nt(S);
+  int fb = fb_max;
+  while (fb > 1 && (fb > F || fb * nt > 64 || das_smem_bytes(fb, S, 0) > 113 * 1024)) fb >>= 1;
+  return fb;
 }
 
-template <int FB, bool T0>
-static cudaError_t launch_fb(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
+template <int FB, int NT, bool T0>
+static cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
   const size_t smem = das_smem_bytes(FB, a.S, a.fir_taps);
-  cudaError_t e = cudaFuncSetAttribute(das_fused_kernel<FB, T0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = das_fused_kernel<FB, NT, T0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.L, (a.F + FB - 1) / FB);
-  das_fused_kernel<FB, T0><<<grid, 288, smem, st>>>(tm, a);
+  kern<<<grid, 256, smem, st>>>(tm, a);
   return cudaGetLastError();
 }
 
 template <bool T0>
 static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, int fb, cudaStream_t st) {
+  const int nt = das_nt(a.S);
   switch (fb) {
-    case 8: return launch_fb<8, T0>(tm, a, st);
-    case 4: return launch_fb<4, T0>(tm, a, st);
-    case 2: return launch_fb<2, T0>(tm, a, st);
-    default: return launch_fb<1, T0>(tm, a, st);
+    case 8: return nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st);
+    case 4:
+      return nt == 4 ? launch_k<4, 4, T0>(tm, a, st)
+                     : (nt == 8 ? launch_k<4, 8, T0>(tm, a, st) : launch_k<4, 16, T0>(tm, a, st));
+    case 2:
+      return nt == 4 ? launch_k<2, 4, T0>(tm, a, st)
+                     : (nt == 8 ? launch_k<2, 8, T0>(tm, a, st) : launch_k<2, 16, T0>(tm, a, st));
+    default:
+      return nt == 4 ? launch_k<1, 4, T0>(tm, a, st)
+                     : (nt == 8 ? launch_k<1, 8, T0>(tm, a, st) : launch_k<1, 16, T0>(tm, a, st));
   }
-}
-
-int das_frames_per_cta(int fb, int F) {
-  while (fb > 1 && fb > F) fb >>= 1;
-  return fb;
 }
 
 cudaError_t launch_das(const CUtensorMap& tm, const DasArgs& a, int fb, cudaStream_t st) {

@@ -63,7 +63,8 @@ struct supra_bf {
   // device tables
   int32_t* d_line_group = nullptr;
   DasEntry* d_entries = nullptr;
-  int32_t* d_ntile = nullptr;
+  int32_t* d_nentries = nullptr;
+  uint16_t* d_ncount = nullptr;
   float4* d_line_dir = nullptr;
   int32_t* d_line_event = nullptr;
   float2* d_fir = nullptr;
@@ -93,7 +94,7 @@ cudaError_t upload(T** d, const std::vector<T>& h) {
 }
 
 void free_all(supra_bf* h) {
-  void* ptrs[] = {h->d_line_group, h->d_entries, h->d_ntile, h->d_line_dir, h->d_line_event,
+  void* ptrs[] = {h->d_line_group, h->d_entries, h->d_nentries, h->d_ncount, h->d_line_dir, h->d_line_event,
                   h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_rows, h->d_ent};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -135,8 +136,9 @@ supra_status validate(const supra_bf_config* c) {
   if (!(c->pitch_x_mm > 0) || !(c->pitch_y_mm > 0)) return fail(SUPRA_E_PARAM, "pitch must be > 0");
   if (!(c->center_frequency_hz > 0)) return fail(SUPRA_E_PARAM, "center_frequency must be > 0");
   if (c->num_events < 1) return fail(SUPRA_E_PARAM, "num_events must be >= 1");
-  if (c->samples_per_channel < 16 || c->samples_per_channel % 8 != 0)
-    return fail(SUPRA_E_PARAM, "samples_per_channel must be >= 16 and a multiple of 8");
+  if (c->samples_per_channel < 32 || c->samples_per_channel % kRowSamples != 0 ||
+      c->samples_per_channel > kMaxSamples)
+    return fail(SUPRA_E_PARAM, "samples_per_channel must be a multiple of 32 in [32, 4096]");
   if (c->input_type != SUPRA_T_I16) return fail(SUPRA_E_PARAM, "input_type must be SUPRA_T_I16");
   if (!(c->sample_frequency_hz > 0)) return fail(SUPRA_E_PARAM, "sample_frequency must be > 0");
   if (!(c->speed_of_sound_mps >= 1000.0 && c->speed_of_sound_mps <= 2000.0))
@@ -271,7 +273,8 @@ supra_status build_das_tables(supra_bf* h) {
   h->entries_per_group = per;
   h->ntiles = (S + kTileK - 1) / kTileK;
   std::vector<DasEntry> flat((size_t)G * per);
-  std::vector<int32_t> ntile((size_t)G * h->ntiles);
+  std::vector<int32_t> nentries(G);
+  std::vector<uint16_t> ncount((size_t)G * S);
   for (int g = 0; g < G; g++) {
     for (int j = 0; j < per; j++) {
       DasEntry d{};
@@ -279,11 +282,12 @@ supra_status build_das_tables(supra_bf* h) {
       else { d.kenter = 0x7fffffff; }
       flat[(size_t)g * per + j] = d;
     }
-    for (int t = 0; t < h->ntiles; t++) {
-      int klast = std::min((t + 1) * kTileK, S) - 1;
-      int n = 0;
-      for (auto& d : groups[g]) n += (d.kenter <= klast);
-      ntile[(size_t)g * h->ntiles + t] = n;
+    nentries[g] = (int)groups[g].size();
+    // N(k) = #entries with k_enter <= k (the aperture count of reading #7)
+    size_t j = 0;
+    for (int k = 0; k < S; k++) {
+      while (j < groups[g].size() && groups[g][j].kenter <= k) j++;
+      ncount[(size_t)g * S + k] = (uint16_t)j;
     }
   }
   std::vector<float4> dirs(L);
@@ -318,7 +322,8 @@ supra_status build_das_tables(supra_bf* h) {
   }
   cudaError_t e;
   if ((e = upload(&h->d_line_group, line_group)) != cudaSuccess ||
-      (e = upload(&h->d_entries, flat)) != cudaSuccess || (e = upload(&h->d_ntile, ntile)) != cudaSuccess ||
+      (e = upload(&h->d_entries, flat)) != cudaSuccess || (e = upload(&h->d_nentries, nentries)) != cudaSuccess ||
+      (e = upload(&h->d_ncount, ncount)) != cudaSuccess ||
       (e = upload(&h->d_line_dir, dirs)) != cudaSuccess || (e = upload(&h->d_line_event, ev)) != cudaSuccess ||
       (e = upload(&h->d_fir, fir)) != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "table upload: %s",
@@ -483,16 +488,19 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// raw [F][E][C][S] int16 viewed as u32 sample pairs {S/2, C, E, F}; box
-// {kWin/2, 1, 1, fb}; out-of-bounds elements read as zero.
+// raw [F][E][C][S] int16 viewed as u32 sample pairs in rows of 16 pairs:
+// dims {16, S/32, C, E, F}; box {16, das_rows(S), 1, 1, fb} -- one TMA per
+// (aperture entry, frame group) fetches a whole trace; out-of-bounds rows
+// (before 0 or past S) and frames (>= F) read as zero.
 bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, int fb) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)S / 2, (cuuint64_t)C, (cuuint64_t)E, (cuuint64_t)F};
-  cuuint64_t strides[3] = {(cuuint64_t)S * 2, (cuuint64_t)C * S * 2, (cuuint64_t)E * C * S * 2};
-  cuuint32_t box[4] = {(cuuint32_t)(kWin / 2), 1, 1, (cuuint32_t)fb};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<void*>(raw), dims, strides, box, es,
+  cuuint64_t dims[5] = {16, (cuuint64_t)S / kRowSamples, (cuuint64_t)C, (cuuint64_t)E, (cuuint64_t)F};
+  cuuint64_t strides[4] = {(cuuint64_t)kRowSamples * 2, (cuuint64_t)S * 2, (cuuint64_t)C * S * 2,
+                           (cuuint64_t)E * C * S * 2};
+  cuuint32_t box[5] = {16, (cuuint32_t)das_rows(S), 1, 1, (cuuint32_t)fb};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<void*>(raw), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -560,10 +568,10 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   }
   // DAS launch shape
   const int maxF = cfg->max_frames_per_call;
-  h->frames_per_cta = das_max_frames_per_cta(h->S, cfg->fir_taps, maxF);
+  h->frames_per_cta = das_frames_per_cta(8, h->S, maxF);
   if (const char* ev = std::getenv("SUPRA_BF_FRAMES_PER_CTA")) {
     int v = std::atoi(ev);
-    if (v == 1 || v == 2 || v == 4 || v == 8) h->frames_per_cta = std::min(v, 8);
+    if (v == 1 || v == 2 || v == 4 || v == 8) h->frames_per_cta = das_frames_per_cta(v, h->S, maxF);
   }
   h->das_smem = das_smem_bytes(h->frames_per_cta, h->S, cfg->fir_taps);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
@@ -607,9 +615,11 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
   a.L = h->L;
   a.ntiles = h->ntiles;
   a.entries_per_group = h->entries_per_group;
+  a.rows = das_rows(h->S);
   a.line_group = h->d_line_group;
   a.entries = h->d_entries;
-  a.ntile = h->d_ntile;
+  a.nentries = h->d_nentries;
+  a.ncount = h->d_ncount;
   a.line_dir = h->d_line_dir;
   a.line_event = h->d_line_event;
   a.t0fs = (float)(c.t0_s * c.sample_frequency_hz);
@@ -636,7 +646,7 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
-  const int fb = das_frames_per_cta(h->frames_per_cta, frames);
+  const int fb = das_frames_per_cta(h->frames_per_cta, h->S, frames);
   CUtensorMap tm;
   if (!make_raw_map(&tm, raw, frames, h->E, h->C, h->S, fb))
     return fail(SUPRA_E_CUDA, "cuTensorMapEncodeTiled failed for the raw buffer");

@@ -9,21 +9,25 @@
 
 namespace supra {
 
-// Depth tile of the DAS kernel: one output sample per consumer thread.
+// DAS kernel geometry.  A consumer thread owns output samples
+// k = kt + kTileK * m (m = 0 .. NT-1) of its line.
 constexpr int kTileK = 256;
-// Staged window per (entry, frame): tile + delay spread margin, in samples.
-// floor tau(k1) - floor tau(k0) <= k1 - k0 + 1 (d tau/dk in [0,1]); the
-// window adds 2 + 3 samples of safety margin and up to 7 + 7 of 16-byte
-// alignment on either end: <= kTileK + 20.
-constexpr int kWin = kTileK + 24;
-// Stages in the bulk-copy ring.
-constexpr int kStages = 4;
-// Producer lanes == bulk copies per stage (entries-per-stage x frames-per-CTA).
-constexpr int kCopiesPerStage = 32;
+// Staged traces are fetched in rows of kRowSamples samples (the 5-D tensor
+// map splits the time axis into rows so one TMA box covers a whole trace).
+constexpr int kRowSamples = 32;
+// Stages in the trace ring (one aperture entry per stage).
+constexpr int kStages = 3;
 // FIR half-length limit (fir_taps <= 2*kMaxHalfTaps + 1 = 129).
 constexpr int kMaxHalfTaps = 64;
-// Rolling RF ring of the fused epilogue: 4 depth tiles.
-constexpr int kRing = 4 * kTileK;
+// Largest record the DAS kernel holds per line (NT = 16 tiles).
+constexpr int kMaxSamples = 16 * kTileK;
+// Output tiles per thread (a template parameter of the DAS kernel) and the
+// trace rows one TMA box fetches for that NT (the stage's frame stride).
+inline __host__ __device__ int das_nt(int S) {
+  const int t = (S + kTileK - 1) / kTileK;
+  return t <= 4 ? 4 : (t <= 8 ? 8 : 16);
+}
+inline __host__ __device__ int das_rows(int S) { return das_nt(S) * (kTileK / kRowSamples) + 2; }
 
 // One receive-aperture entry of a line group (lines sharing an origin),
 // sorted by k_enter.  Lengths in "sample units" (mm * fs / (1000 c)), in
@@ -41,10 +45,12 @@ struct DasArgs {
   const int16_t* raw;      // [F][E][C][S]
   int F, E, C, S, L;
   int ntiles;              // ceil(S / kTileK)
-  int entries_per_group;   // padded to a multiple of 32
+  int entries_per_group;   // row stride of `entries`
+  int rows;                // trace rows per TMA box: S / kRowSamples + 2
   const int32_t* line_group;   // [L]
-  const DasEntry* entries;     // [G][entries_per_group]
-  const int32_t* ntile;        // [G][ntiles]: entries with kenter <= last k of tile
+  const DasEntry* entries;     // [G][entries_per_group], sorted by kenter
+  const int32_t* nentries;     // [G]: entries with kenter < S
+  const uint16_t* ncount;      // [G][S]: N(k) = #entries with kenter <= k
   const float4* line_dir;      // [L] (dx, dy, dz, 0)
   const int32_t* line_event;   // [L]
   float t0fs;                  // t0 * fs (samples)
@@ -128,12 +134,11 @@ struct ScArgs {
 };
 
 // Launchers (return cudaGetLastError()).
-// raw is addressed through a 4-D tensor map {S/2 sample pairs (u32), C, E, F}
-// with box {kWin/2, 1, 1, fb}; fb = das_frames_per_cta(configured, F).
+// raw is addressed through a 5-D tensor map {16 sample pairs (u32), S/32
+// rows, C, E, F} with box {16, rows, 1, 1, fb}; fb = das_frames_per_cta().
 cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, int fb, cudaStream_t st);
-int das_frames_per_cta(int fb, int F);
+int das_frames_per_cta(int fb_max, int S, int F);
 size_t das_smem_bytes(int frames_per_cta, int S, int fir_taps);
-int das_max_frames_per_cta(int S, int fir_taps, int F);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st);
