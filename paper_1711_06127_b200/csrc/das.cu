@@ -134,38 +134,38 @@ __host__ __device__ inline size_t fir_bytes(int FB, int S) {
 
 struct SmemLayout {
   int16_t* stage;   // [kStages][stage_bytes]
-  float4* rec;      // [kStages] {Ah, B, pi*cu, k_enter bits}
-  int* ws;          // [kStages]
+  float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
+  int2* wse;        // [nent] {window start ws, channel}
   uint64_t* full;   // [kStages]
-  uint64_t* empty;  // [kStages]
+  unsigned* rel;    // [kStages] warps done with the slot (last one refills it)
   unsigned* smax;   // [8]
   float4* line;     // FIR buffer, aliases the stage ring after the DAS loop
 };
 
-__host__ __device__ inline size_t layout_bytes(int FB, int S, size_t* off) {
+__host__ __device__ inline size_t layout_bytes(int FB, int S, int nent_max, size_t* off) {
   const int rows = das_rows(S);
   const size_t ring = (size_t)kStages * stage_bytes(FB, rows);
   const size_t fb = fir_bytes(FB, S);
   size_t o = 0;
   off[0] = o; o = align128(o + (ring > fb ? ring : fb));
-  off[1] = o; o = align128(o + sizeof(float4) * kStages);
-  off[2] = o; o = align128(o + sizeof(int) * kStages);
+  off[1] = o; o = align128(o + sizeof(float4) * nent_max);
+  off[2] = o; o = align128(o + sizeof(int2) * nent_max);
   off[3] = o; o = align128(o + sizeof(uint64_t) * kStages);
-  off[4] = o; o = align128(o + sizeof(uint64_t) * kStages);
+  off[4] = o; o = align128(o + sizeof(unsigned) * kStages);
   off[5] = o; o = align128(o + sizeof(unsigned) * 8);
   return o;
 }
 
-__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int S) {
+__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int S, int nent_max) {
   size_t off[6];
-  layout_bytes(FB, S, off);
+  layout_bytes(FB, S, nent_max, off);
   SmemLayout L;
   L.stage = (int16_t*)(base + off[0]);
   L.line = (float4*)(base + off[0]);
   L.rec = (float4*)(base + off[1]);
-  L.ws = (int*)(base + off[2]);
+  L.wse = (int2*)(base + off[2]);
   L.full = (uint64_t*)(base + off[3]);
-  L.empty = (uint64_t*)(base + off[4]);
+  L.rel = (unsigned*)(base + off[4]);
   L.smax = (unsigned*)(base + off[5]);
   return L;
 }
@@ -315,52 +315,54 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
   const int S = a.S;
   constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
   const size_t SB = stage_bytes(FB, NT * 8 + 2);
-  SmemLayout sm = carve(smem_raw, FB, S);
+  SmemLayout sm = carve(smem_raw, FB, S, a.entries_per_group);
   const int line = blockIdx.x;
   const int f0 = blockIdx.y * FB;
   const int g = a.line_group[line];
   const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
   const int nent = a.nentries[g];
   const int lane = threadIdx.x & 31;
+  const int ev = a.line_event[line];
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; i++) {
       mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 8);
+      sm.rel[i] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   if (threadIdx.x < 8) sm.smax[threadIdx.x] = 0u;
+  // Entry records for this line, computed once in parallel:
+  // window [ws, ws + rows*32), rows = 8 NT + 2 >= S/32 + 2,
+  // ws <= floor(tau(k_enter)) - 2 and 32-aligned: d tau/dk in [0, 1] gives
+  // i0(k) + 1 <= ws + S + 34 for every member k < S, inside the window;
+  // reads past the record (>= S) or before it (< 0) come back as TMA zeros.
+  {
+    const float4 dir = a.line_dir[line];
+    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
+      const DasEntry e = ents[i];
+      const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
+      const float Ah = 0.5f * e.A;
+      const int kb = e.kenter;
+      const float hb = 0.5f * (float)kb;
+      const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
+      const int ws = ((int)floorf(tb) - 2) & ~(kRowSamples - 1);
+      sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(kb));
+      sm.wse[i] = make_int2(ws, e.elem);
+    }
+  }
   __syncthreads();
 
-  // Producer role (thread 0, inline): issue the TMA of entry jj into ring
-  // slot jj % kStages once every warp has released that slot.
-  const int ev = a.line_event[line];
-  const float4 dir = a.line_dir[line];
+  // Producer step: TMA of entry jj's trace (all FB frames) into slot jj % kStages.
   auto produce = [&](int jj) {
     const int buf = jj % kStages;
-    if (jj >= kStages) mbar_wait(&sm.empty[buf], ((jj / kStages) - 1) & 1);
-    const DasEntry e = ents[jj];
-    const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
-    const float Ah = 0.5f * e.A;
-    const int kb = e.kenter;
-    const float hb = 0.5f * (float)kb;
-    const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
-    // window [ws, ws + rows*32), rows = S/32 + 2, ws <= floor(tau(k_enter)) - 2
-    // and 32-aligned: d tau/dk in [0, 1] gives i0(k) + 1 <= ws + S + 34
-    // for every member k < S, inside the window; reads past the record
-    // (>= S) or before it (< 0) come back as TMA zeros.
-    const int ws = ((int)floorf(tb) - 2) & ~(kRowSamples - 1);
-    sm.rec[buf] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(kb));
-    sm.ws[buf] = ws;
+    const int2 we = sm.wse[jj];
     mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
-    tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, ws / kRowSamples, e.elem, ev, f0,
-                &sm.full[buf]);
+    tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, we.x / kRowSamples, we.y, ev, f0, &sm.full[buf]);
   };
-  if (threadIdx.x == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-    for (int jj = 0; jj < kStages - 1 && jj < nent; jj++) produce(jj);
-  }
+  if (threadIdx.x == 0)
+    for (int jj = 0; jj < kStages && jj < nent; jj++) produce(jj);
 
   {
     // ------------------------------ consumers -----------------------------
@@ -369,20 +371,32 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
     Acc<FB, NT> acc;
     acc.zero();
     for (int j = 0; j < nent; j++) {
-      if (threadIdx.x == 0 && j + kStages - 1 < nent) produce(j + kStages - 1);
       const int buf = j % kStages;
       mbar_wait(&sm.full[buf], (j / kStages) & 1);
-      const float4 r = sm.rec[buf];
+      const float4 r = sm.rec[j];
       const int kenter = __float_as_int(r.w);
-      const int wsm = sm.ws[buf] + kFloorMagicBits - kt;
+      const int wsm = sm.wse[j].x + kFloorMagicBits - kt;
       const unsigned short* st = (const unsigned short*)((const unsigned char*)sm.stage + buf * SB);
       // straight-line code for the tiles at or after the entry's first
       // active tile (no per-tile branches: the chains of consecutive tiles
       // interleave)
       dispatch_tiles<FB, NT, T0>(min(kenter / kTileK, NT - 1) / tile_gran(NT), a, r, kenter, wsm, st, kt, ktf, S,
                                  acc);
+      // release the slot; the last warp to release it refills it (no warp
+      // ever waits for another to issue a copy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[buf]);
+      if (lane == 0) {
+        __threadfence_block();
+        const unsigned prev = atomicAdd(&sm.rel[buf], 1u);
+        if (prev == (blockDim.x / 32) - 1) {
+          __threadfence_block();
+          sm.rel[buf] = 0u;
+          if (j + kStages < nent) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            produce(j + kStages);
+          }
+        }
+      }
     }
     // ---- RF = sum / N (reading #7; 0 when N = 0) ----
     const uint16_t* ncount = a.ncount + (size_t)g * S;
@@ -456,23 +470,23 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
   }
 }
 
-size_t das_smem_bytes(int FB, int S, int) {
+size_t das_smem_bytes(int FB, int S, int nent_max) {
   size_t off[6];
-  return layout_bytes(FB, S, off);
+  return layout_bytes(FB, S, nent_max, off);
 }
 
 // Frames per CTA: registers hold NT x FB accumulators (<= 64), the smem
 // footprint must allow 2 CTAs per SM, and never more frames than the call.
-int das_frames_per_cta(int fb_max, int S, int F) {
+int das_frames_per_cta(int fb_max, int S, int F, int nent_max) {
   const int nt = das_nt(S);
   int fb = fb_max;
-  while (fb > 1 && (fb > F || fb * nt > 64 || das_smem_bytes(fb, S, 0) > 113 * 1024)) fb >>= 1;
+  while (fb > 1 && (fb > F || fb * nt > 64 || das_smem_bytes(fb, S, nent_max) > 113 * 1024)) fb >>= 1;
   return fb;
 }
 
 template <int FB, int NT, bool T0>
 static cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
-  const size_t smem = das_smem_bytes(FB, a.S, a.fir_taps);
+  const size_t smem = das_smem_bytes(FB, a.S, a.entries_per_group);
   auto kern = das_fused_kernel<FB, NT, T0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -568,12 +568,12 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   }
   // DAS launch shape
   const int maxF = cfg->max_frames_per_call;
-  h->frames_per_cta = das_frames_per_cta(8, h->S, maxF);
+  h->frames_per_cta = das_frames_per_cta(8, h->S, maxF, h->entries_per_group);
   if (const char* ev = std::getenv("SUPRA_BF_FRAMES_PER_CTA")) {
     int v = std::atoi(ev);
-    if (v == 1 || v == 2 || v == 4 || v == 8) h->frames_per_cta = das_frames_per_cta(v, h->S, maxF);
+    if (v == 1 || v == 2 || v == 4 || v == 8) h->frames_per_cta = das_frames_per_cta(v, h->S, maxF, h->entries_per_group);
   }
-  h->das_smem = das_smem_bytes(h->frames_per_cta, h->S, cfg->fir_taps);
+  h->das_smem = das_smem_bytes(h->frames_per_cta, h->S, h->entries_per_group);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
   if (e == cudaSuccess && cfg->reference_mode == SUPRA_REF_FRAME_MAX && cfg->line_output_type == SUPRA_T_U8)
     e = cudaMalloc((void**)&h->d_env, sizeof(float) * (size_t)maxF * h->L * h->S);
@@ -646,7 +646,7 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
-  const int fb = das_frames_per_cta(h->frames_per_cta, h->S, frames);
+  const int fb = das_frames_per_cta(h->frames_per_cta, h->S, frames, h->entries_per_group);
   CUtensorMap tm;
   if (!make_raw_map(&tm, raw, frames, h->E, h->C, h->S, fb))
     return fail(SUPRA_E_CUDA, "cuTensorMapEncodeTiled failed for the raw buffer");

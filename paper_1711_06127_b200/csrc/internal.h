@@ -137,8 +137,8 @@ struct ScArgs {
 // raw is addressed through a 5-D tensor map {16 sample pairs (u32), S/32
 // rows, C, E, F} with box {16, rows, 1, 1, fb}; fb = das_frames_per_cta().
 cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, int fb, cudaStream_t st);
-int das_frames_per_cta(int fb_max, int S, int F);
-size_t das_smem_bytes(int frames_per_cta, int S, int fir_taps);
+int das_frames_per_cta(int fb_max, int S, int F, int nent_max);
+size_t das_smem_bytes(int frames_per_cta, int S, int nent_max);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st);
