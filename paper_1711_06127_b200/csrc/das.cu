@@ -53,13 +53,21 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
       : "memory");
 }
 
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or ~the hint elapses) instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
+}
+
+__device__ __forceinline__ unsigned atom_add_shared(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
 }
 
 // 5-D TMA tile load: box {16 pairs, rows, 1 channel, 1 event, FB frames}.
@@ -132,26 +140,32 @@ __host__ __device__ inline size_t fir_bytes(int FB, int S) {
   return align128((size_t)((FB + 3) / 4) * fir_span(S) * 16);
 }
 
+// Stages in the trace ring: as many as fit a ~100 KB budget (2 CTAs/SM), 3..8.
+__host__ __device__ inline int das_stages(int FB, int S) {
+  const int n = (int)((100 * 1024) / stage_bytes(FB, das_rows(S)));
+  return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : n);
+}
+
 struct SmemLayout {
-  int16_t* stage;   // [kStages][stage_bytes]
+  int16_t* stage;   // [NS][stage_bytes]
   float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
   int2* wse;        // [nent] {window start ws, channel}
-  uint64_t* full;   // [kStages]
-  unsigned* rel;    // [kStages] warps done with the slot (last one refills it)
+  uint64_t* full;   // [NS]
+  unsigned* rel;    // [NS] warps done with the slot (last one refills it)
   unsigned* smax;   // [8]
   float4* line;     // FIR buffer, aliases the stage ring after the DAS loop
 };
 
 __host__ __device__ inline size_t layout_bytes(int FB, int S, int nent_max, size_t* off) {
   const int rows = das_rows(S);
-  const size_t ring = (size_t)kStages * stage_bytes(FB, rows);
+  const size_t ring = (size_t)das_stages(FB, S) * stage_bytes(FB, rows);
   const size_t fb = fir_bytes(FB, S);
   size_t o = 0;
   off[0] = o; o = align128(o + (ring > fb ? ring : fb));
   off[1] = o; o = align128(o + sizeof(float4) * nent_max);
   off[2] = o; o = align128(o + sizeof(int2) * nent_max);
-  off[3] = o; o = align128(o + sizeof(uint64_t) * kStages);
-  off[4] = o; o = align128(o + sizeof(unsigned) * kStages);
+  off[3] = o; o = align128(o + sizeof(uint64_t) * kMaxStages);
+  off[4] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
   off[5] = o; o = align128(o + sizeof(unsigned) * 8);
   return o;
 }
@@ -266,7 +280,11 @@ __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, i
 #pragma unroll
   for (int m = M0; m < NT; m++) {
     const int k = m * kTileK + kt;
-    const bool mem = (k >= kenter) && (k < S);
+    // k_enter < (M0 + gran) * 256, so only the first gran tiles can hold
+    // non-members.  Outputs k >= S (when S < 256 NT) are computed but never
+    // stored, and their taps stay inside the staged window.
+    const bool first = m < M0 + tile_gran(NT);
+    const bool mem = !first || k >= kenter;
     const float kf = ktf + (float)(m * kTileK);
     const float h = 0.5f * kf;
     const float h2 = (m == 0 && kt == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
@@ -276,6 +294,9 @@ __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, i
     int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - kt)
     const float fr = delta - (tf - kFloorMagic);
     idx = mem ? idx : 0;
+    // opaque copy: keeps one materialised index so the 2 FB loads below use
+    // immediate offsets instead of one address add each
+    asm("mov.b32 %0, %0;" : "+r"(idx));
     float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
     w = mem ? w : 0.f;
     const float wf = w * fr;
@@ -324,8 +345,9 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
   const int lane = threadIdx.x & 31;
   const int ev = a.line_event[line];
 
+  const int NS = das_stages(FB, S);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; i++) {
+    for (int i = 0; i < NS; i++) {
       mbar_init(&sm.full[i], 1);
       sm.rel[i] = 0u;
     }
@@ -354,15 +376,14 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
   }
   __syncthreads();
 
-  // Producer step: TMA of entry jj's trace (all FB frames) into slot jj % kStages.
-  auto produce = [&](int jj) {
-    const int buf = jj % kStages;
+  // Producer step: TMA of entry jj's trace (all FB frames) into slot buf.
+  auto produce = [&](int jj, int buf) {
     const int2 we = sm.wse[jj];
     mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
     tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, we.x / kRowSamples, we.y, ev, f0, &sm.full[buf]);
   };
   if (threadIdx.x == 0)
-    for (int jj = 0; jj < kStages && jj < nent; jj++) produce(jj);
+    for (int jj = 0; jj < NS && jj < nent; jj++) produce(jj, jj);
 
   {
     // ------------------------------ consumers -----------------------------
@@ -370,9 +391,10 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
     const float ktf = (float)kt;
     Acc<FB, NT> acc;
     acc.zero();
+    int buf = 0;
+    unsigned phase = 0;
     for (int j = 0; j < nent; j++) {
-      const int buf = j % kStages;
-      mbar_wait(&sm.full[buf], (j / kStages) & 1);
+      mbar_wait(&sm.full[buf], phase);
       const float4 r = sm.rec[j];
       const int kenter = __float_as_int(r.w);
       const int wsm = sm.wse[j].x + kFloorMagicBits - kt;
@@ -387,15 +409,19 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
-        const unsigned prev = atomicAdd(&sm.rel[buf], 1u);
+        const unsigned prev = atom_add_shared(&sm.rel[buf], 1u);
         if (prev == (blockDim.x / 32) - 1) {
           __threadfence_block();
           sm.rel[buf] = 0u;
-          if (j + kStages < nent) {
+          if (j + NS < nent) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            produce(j + kStages);
+            produce(j + NS, buf);
           }
         }
+      }
+      if (++buf == NS) {
+        buf = 0;
+        phase ^= 1u;
       }
     }
     // ---- RF = sum / N (reading #7; 0 when N = 0) ----

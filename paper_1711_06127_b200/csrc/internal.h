@@ -15,8 +15,8 @@ constexpr int kTileK = 256;
 // Staged traces are fetched in rows of kRowSamples samples (the 5-D tensor
 // map splits the time axis into rows so one TMA box covers a whole trace).
 constexpr int kRowSamples = 32;
-// Stages in the trace ring (one aperture entry per stage).
-constexpr int kStages = 3;
+// Maximum stages in the trace ring (one aperture entry per stage).
+constexpr int kMaxStages = 8;
 // FIR half-length limit (fir_taps <= 2*kMaxHalfTaps + 1 = 129).
 constexpr int kMaxHalfTaps = 64;
 // Largest record the DAS kernel holds per line (NT = 16 tiles).
