@@ -62,8 +62,9 @@ enum { SUPRA_SC_LINEAR_2D = 0, SUPRA_SC_SECTOR_2D = 1, SUPRA_SC_PYRAMID_3D = 2 }
  * Configuration.  `supra_bf_create` copies every field and array; the caller
  * may free them afterwards.  Ranges checked at create (else SUPRA_E_PARAM):
  *   elements_x, elements_y >= 1, pitch > 0, center_frequency > 0;
- *   num_events >= 1; samples_per_channel >= 16 and a multiple of 8 (16-byte
- *   rows for the bulk-copy staging); input_type = SUPRA_T_I16;
+ *   num_events >= 1; samples_per_channel a multiple of 32 in [32, 4096]
+ *   (one TMA box holds a whole trace in 64-byte rows; 4096 = 16 tiles of 256
+ *   samples held in registers per thread); input_type = SUPRA_T_I16;
  *   sample_frequency > 0; speed_of_sound in [1000, 2000];
  *   f_number > 0; window, normalize in their enums;
  *   fir_taps odd, 1..129; decimation = 1 (>1 is future work);
@@ -142,7 +143,8 @@ supra_status supra_bf_create(const supra_bf_config *cfg, supra_bf_t *out);
  *   y = 0 if env = 0, else clamp((20 log10(env/ref) + DR)/DR, 0, 1),
  *   ref = per-frame max of env (SUPRA_REF_FRAME_MAX) or reference_value.
  * Arguments:
- *   raw      : device, int16 [frames][num_events][channels][samples], 16-byte aligned.
+ *   raw      : device, int16 [frames][num_events][channels][samples], 16-byte aligned
+ *              (read through a TMA tensor map encoded per call).
  *   frames   : 0 .. max_frames_per_call (0 = no-op).
  *   rf       : device float [frames][L][samples] or NULL.
  *   line_img : device [frames][L][samples] of line_output_type or NULL
@@ -208,6 +210,15 @@ supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t *valid, int32_t *idx);
  *   pixels, [7] kernels per scanconvert call.
  */
 supra_status supra_bf_info(supra_bf_t h, int64_t *info8);
+
+/*
+ * supra_bf_set_das_events -- measurement hook for the bench: when non-NULL,
+ * supra_bf_beamform records `before` and `after` (cudaEvent_t) on its stream
+ * immediately around the DAS kernel launch, so the kernel's duration can be
+ * timed with CUDA events on the stream it runs on.  NULL, NULL disables.
+ * Errors: SUPRA_E_STRUCT on a NULL handle.
+ */
+supra_status supra_bf_set_das_events(supra_bf_t h, void *before, void *after);
 
 #ifdef __cplusplus
 }

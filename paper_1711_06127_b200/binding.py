@@ -25,7 +25,8 @@ T_I16, T_F32, T_U8 = 0, 1, 2
 SC_LINEAR_2D, SC_SECTOR_2D, SC_PYRAMID_3D = 0, 1, 2
 
 EXPORTS = ("supra_bf_create", "supra_bf_beamform", "supra_bf_envelope_log", "supra_bf_scanconvert",
-           "supra_bf_destroy", "supra_bf_last_error", "supra_bf_sc_indices", "supra_bf_info")
+           "supra_bf_destroy", "supra_bf_last_error", "supra_bf_sc_indices", "supra_bf_info",
+           "supra_bf_set_das_events")
 
 
 class SupraError(RuntimeError):
@@ -89,6 +90,8 @@ def lib():
         L.supra_bf_sc_indices.restype = C.c_int
         L.supra_bf_info.argtypes = [vp, vp]
         L.supra_bf_info.restype = C.c_int
+        L.supra_bf_set_das_events.argtypes = [vp, vp, vp]
+        L.supra_bf_set_das_events.restype = C.c_int
         _lib = L
     return _lib
 
@@ -189,6 +192,12 @@ class SupraBF:
         keys = ("kernels_per_beamform", "frames_per_cta", "tile_k", "referenced_bytes_per_frame",
                 "taps_per_frame", "sc_table_bytes", "sc_valid_pixels", "kernels_per_scanconvert")
         return {k: int(v) for k, v in zip(keys, a)}
+
+    def set_das_events(self, before=None, after=None):
+        """Record torch.cuda.Event ``before``/``after`` around the DAS launch."""
+        b = None if before is None else before.cuda_event
+        a = None if after is None else after.cuda_event
+        _check(lib().supra_bf_set_das_events(self.h, b, a))
 
     def sc_indices(self):
         n = int(np.prod(self.w.out_dims))

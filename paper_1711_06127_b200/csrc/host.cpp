@@ -79,6 +79,7 @@ struct supra_bf {
   std::vector<ScRow> h_rows;
   std::vector<ScEntry> h_ent;
   std::vector<float> fir_c, fir_s;
+  cudaEvent_t ev_before = nullptr, ev_after = nullptr;
   int64_t info[8] = {0};
 };
 
@@ -597,6 +598,13 @@ void supra_bf_destroy(supra_bf_t h) {
   delete h;
 }
 
+supra_status supra_bf_set_das_events(supra_bf_t h, void* before, void* after) {
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  h->ev_before = (cudaEvent_t)before;
+  h->ev_after = (cudaEvent_t)after;
+  return SUPRA_OK;
+}
+
 supra_status supra_bf_info(supra_bf_t h, int64_t* info8) {
   if (!h || !info8) return fail(SUPRA_E_STRUCT, "NULL argument");
   std::memcpy(info8, h->info, sizeof h->info);
@@ -650,7 +658,9 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
   CUtensorMap tm;
   if (!make_raw_map(&tm, raw, frames, h->E, h->C, h->S, fb))
     return fail(SUPRA_E_CUDA, "cuTensorMapEncodeTiled failed for the raw buffer");
+  if (h->ev_before) cudaEventRecord(h->ev_before, st);
   supra_status s = check_launch(launch_das(tm, a, fb, st), "das kernel");
+  if (h->ev_after) cudaEventRecord(h->ev_after, st);
   if (s != SUPRA_OK || !line_img || a.ref_fixed) return s;
   FinalizeArgs fa{};
   fa.env = a.env_out;
