@@ -72,6 +72,11 @@ struct supra_bf {
   float* d_env = nullptr;
   ScAxis* d_ax = nullptr;
   ScAxis* d_az = nullptr;
+  int32_t* d_blk_kmin = nullptr;
+  int32_t* d_col_l0 = nullptr;
+  int32_t* d_col_nl = nullptr;
+  int slab_k = 2;
+  int sc_tiled = 1;
   ScRow* d_rows = nullptr;
   ScEntry* d_ent = nullptr;
   // host copies for introspection
@@ -96,7 +101,7 @@ cudaError_t upload(T** d, const std::vector<T>& h) {
 
 void free_all(supra_bf* h) {
   void* ptrs[] = {h->d_line_group, h->d_entries, h->d_nentries, h->d_ncount, h->d_line_dir, h->d_line_event,
-                  h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_rows, h->d_ent};
+                  h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_blk_kmin, h->d_col_l0, h->d_col_nl, h->d_rows, h->d_ent};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -410,6 +415,41 @@ supra_status build_sc_tables(supra_bf* h) {
       vz += ok;
     }
     nvalid = vx * vz;
+    // per block of kScRows output rows: the k range its valid rows touch
+    const int nb = (nz + kScRows - 1) / kScRows;
+    std::vector<int32_t> kmin(nb, -1);
+    int span = 2;
+    for (int b = 0; b < nb; b++) {
+      int lo = -1, hi = -1;
+      for (int iz = b * kScRows; iz < std::min(nz, (b + 1) * kScRows); iz++) {
+        int k0 = h->h_az[iz].i0;
+        if (k0 < 0) continue;
+        if (lo < 0 || k0 < lo) lo = k0;
+        if (k0 > hi) hi = k0;
+      }
+      kmin[b] = lo;
+      if (lo >= 0) span = std::max(span, hi - lo + 2);
+    }
+    h->slab_k = span | 1;  // odd: slab rows of consecutive lines start in distinct banks
+    // per 256-column tile: the lines its valid columns touch (i0 .. i0 + 1)
+    const int nc = (nx + 255) / 256;
+    std::vector<int32_t> cl0(nc, 0), cnl(nc, 0);
+    for (int cb = 0; cb < nc; cb++) {
+      int lo = -1, hi = -1;
+      for (int ix = cb * 256; ix < std::min(nx, (cb + 1) * 256); ix++) {
+        int i0 = h->h_ax[ix].i0;
+        if (i0 < 0) continue;
+        if (lo < 0 || i0 < lo) lo = i0;
+        if (i0 + 1 > hi) hi = i0 + 1;
+      }
+      if (lo >= 0) { cl0[cb] = lo; cnl[cb] = hi - lo + 1; }
+    }
+    int maxnl = 0;
+    for (int v : cnl) maxnl = std::max(maxnl, v);
+    h->sc_tiled = (maxnl <= kScMaxLines && h->slab_k <= kScMaxK) ? 1 : 0;  // else direct kernel
+    if ((e = upload(&h->d_blk_kmin, kmin)) != cudaSuccess || (e = upload(&h->d_col_l0, cl0)) != cudaSuccess ||
+        (e = upload(&h->d_col_nl, cnl)) != cudaSuccess)
+      return fail(SUPRA_E_RESOURCE, "sc upload: %s", cudaGetErrorString(e));
     if ((e = upload(&h->d_ax, h->h_ax)) != cudaSuccess || (e = upload(&h->d_az, h->h_az)) != cudaSuccess)
       return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "sc upload: %s",
                   cudaGetErrorString(e));
@@ -764,6 +804,11 @@ supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t fr
   a.mask = mask;
   a.ax = h->d_ax;
   a.az = h->d_az;
+  a.blk_kmin = h->d_blk_kmin;
+  a.slab_k = h->slab_k;
+  a.col_l0 = h->d_col_l0;
+  a.col_nl = h->d_col_nl;
+  a.tiled = h->sc_tiled;
   a.rows = h->d_rows;
   a.ent = h->d_ent;
   a.is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;

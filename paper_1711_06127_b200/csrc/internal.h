@@ -98,6 +98,13 @@ struct FinalizeArgs {  // frame-max reference: env -> y
   int y_type;
 };
 
+// Linear scan-conversion tile: 256 columns x kScRows rows per CTA; the
+// staged slab holds at most kScMaxLines lines x kScMaxK samples (checked at
+// create: the tile's columns must span <= kScMaxLines - 1 line pitches).
+constexpr int kScRows = 32;
+constexpr int kScMaxLines = 64;
+constexpr int kScMaxK = 64;
+
 // Linear (separable) scan conversion table entries.
 struct ScAxis {
   int32_t i0;   // -1: invalid
@@ -127,6 +134,11 @@ struct ScArgs {
   // linear
   const ScAxis* ax;      // [nx]
   const ScAxis* az;      // [nz]
+  const int32_t* blk_kmin;  // [ceil(nz / kScRows)]: smallest valid k0 of the row block, -1 if none
+  int slab_k;            // samples per line staged per row block
+  const int32_t* col_l0;    // [ceil(nx / 256)]: first line the column tile touches
+  const int32_t* col_nl;    // [ceil(nx / 256)]: lines it touches (0: none valid)
+  int tiled;             // 1: tiled separable kernel; 0: direct per-pixel kernel
   // table
   const ScRow* rows;     // [nz*ny]
   const ScEntry* ent;

@@ -20,6 +20,18 @@ __device__ __forceinline__ float load_y(const void* p, int type, size_t i) {
   return __ldg((const float*)p + i);
 }
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
 __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) {
   if (type == SUPRA_T_U8) ((uint8_t*)p)[i] = (uint8_t)floorf(255.f * v + 0.5f);
   else ((float*)p)[i] = v;
@@ -27,27 +39,100 @@ __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) 
 
 }  // namespace
 
-// grid (ceil(nx/128), nz, F); block 128: one pixel per thread, x fastest.
-__global__ void __launch_bounds__(128) sc_linear_kernel(const ScArgs a) {
-  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
-  const int iz = blockIdx.y, f = blockIdx.z;
-  if (ix >= a.nx) return;
-  const ScAxis ax = a.ax[ix], az = a.az[iz];
-  const bool ok = ax.i0 >= 0 && az.i0 >= 0;
-  float v = 0.f;
-  if (ok) {
-    const size_t L = (size_t)a.Lx;
-    const size_t b = ((size_t)f * L + ax.i0) * a.S + az.i0;
-    const float y00 = load_y(a.line_img, a.in_type, b);
-    const float y01 = load_y(a.line_img, a.in_type, b + 1);
-    const float y10 = load_y(a.line_img, a.in_type, b + a.S);
-    const float y11 = load_y(a.line_img, a.in_type, b + a.S + 1);
-    const float fx = ax.f, fz = az.f;
-    v = (1.f - fz) * ((1.f - fx) * y00 + fx * y10) + fz * ((1.f - fx) * y01 + fx * y11);
+// Linear 2D, tiled and separable: one CTA per (256 output columns x
+// kScRows output rows, frame); one thread per column.  Because u depends
+// only on x and v only on z (reading #21), the bilinear blend factors into a
+// depth lerp per (row, line) followed by a lateral lerp per pixel:
+//   t[r][l] = lerp(y[l][k0], y[l][k0+1], fz(r)),
+//   out[r][x] = lerp(t[r][i0], t[r][i0+1], fx(x)).
+// The slab of the line image the tile touches (lines [l0, l0+nl) x ks
+// samples from the row block's smallest k0, both host-computed) is staged in
+// shared memory with cp.async.
+template <bool U8OUT>
+__global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
+  __shared__ float slab[kScMaxLines * kScMaxK];
+  __shared__ float tz[kScRows * kScMaxLines];
+  __shared__ ScAxis saz[kScRows];
+  const int cb = blockIdx.x, rb = blockIdx.y, f = blockIdx.z;
+  const int x = cb * 256 + threadIdx.x;
+  const int z0 = rb * kScRows;
+  const int ks = a.slab_k;
+  const int kmin = a.blk_kmin[rb];
+  const int l0 = a.col_l0[cb], nl = a.col_nl[cb];
+  const int Lx = a.Lx, S = a.S, nx = a.nx;
+  const int rows = min(kScRows, a.nz - z0);
+  const size_t fbase = (size_t)f * Lx * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (kmin >= 0 && nl > 0) {
+    if (a.in_type == SUPRA_T_F32) {
+      const float* src = (const float*)a.line_img + fbase;
+      for (int l = warp; l < nl; l += 8)
+        for (int kk = lane; kk < ks; kk += 32)
+          cp_async4(slab + l * ks + kk, src + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
+    } else {
+      for (int l = warp; l < nl; l += 8)
+        for (int kk = lane; kk < ks; kk += 32)
+          slab[l * ks + kk] = load_y(a.line_img, a.in_type, fbase + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
+    }
   }
-  const size_t o = (size_t)iz * a.nx + ix;
-  store_img(a.img, a.out_type, (size_t)f * a.nz * a.nx + o, v);
-  if (a.mask && f == 0) a.mask[o] = ok ? 1 : 0;
+  if (threadIdx.x < rows) cp_async8(saz + threadIdx.x, a.az + z0 + threadIdx.x);
+  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+  const ScAxis ax = x < nx ? a.ax[x] : ScAxis{-1, 0.f};
+  __syncthreads();
+  if ((int)threadIdx.x < nl) {
+    const float* y = slab + threadIdx.x * ks - kmin;
+    for (int r = 0; r < rows; r++) {
+      const ScAxis az = saz[r];
+      if (az.i0 >= 0) tz[r * kScMaxLines + threadIdx.x] = fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]);
+    }
+  }
+  __syncthreads();
+  if (x >= nx) return;
+  const bool colok = ax.i0 >= 0;
+  const float* tcol = tz + (colok ? ax.i0 - l0 : 0);
+  const size_t out0 = ((size_t)f * a.nz + z0) * nx + x;
+  if (U8OUT) {
+    uint8_t* o = (uint8_t*)a.img + out0;
+#pragma unroll 4
+    for (int r = 0; r < rows; r++, o += nx) {
+      const bool ok = colok && saz[r].i0 >= 0;
+      const float t0 = tcol[r * kScMaxLines], t1 = tcol[r * kScMaxLines + 1];
+      const float v = ok ? fmaf(ax.f, t1 - t0, t0) : 0.f;
+      *o = (uint8_t)floorf(fmaf(255.f, v, 0.5f));
+    }
+  } else {
+    float* o = (float*)a.img + out0;
+#pragma unroll 4
+    for (int r = 0; r < rows; r++, o += nx) {
+      const bool ok = colok && saz[r].i0 >= 0;
+      const float t0 = tcol[r * kScMaxLines], t1 = tcol[r * kScMaxLines + 1];
+      *o = ok ? fmaf(ax.f, t1 - t0, t0) : 0.f;
+    }
+  }
+  if (a.mask && f == 0)
+    for (int r = 0; r < rows; r++) a.mask[(size_t)(z0 + r) * nx + x] = (colok && saz[r].i0 >= 0) ? 1 : 0;
+}
+
+// Linear 2D, direct (grids too coarse for the tiled kernel's slab): one
+// pixel per thread, gathers through L1.
+__global__ void __launch_bounds__(256) sc_linear_direct_kernel(const ScArgs a) {
+  const size_t n = (size_t)a.nz * a.nx;
+  const int f = blockIdx.y;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
+    const int iz = (int)(p / a.nx), ix = (int)(p - (size_t)iz * a.nx);
+    const ScAxis ax = a.ax[ix], az = a.az[iz];
+    const bool ok = ax.i0 >= 0 && az.i0 >= 0;
+    float v = 0.f;
+    if (ok) {
+      const size_t b = ((size_t)f * a.Lx + ax.i0) * a.S + az.i0;
+      const float y00 = load_y(a.line_img, a.in_type, b), y01 = load_y(a.line_img, a.in_type, b + 1);
+      const float y10 = load_y(a.line_img, a.in_type, b + a.S), y11 = load_y(a.line_img, a.in_type, b + a.S + 1);
+      const float t0 = fmaf(az.f, y01 - y00, y00), t1 = fmaf(az.f, y11 - y10, y10);
+      v = fmaf(ax.f, t1 - t0, t0);
+    }
+    store_img(a.img, a.out_type, (size_t)f * n + p, v);
+    if (a.mask && f == 0) a.mask[p] = ok ? 1 : 0;
+  }
 }
 
 // grid (nz*ny, F); block 256 looping over x.
@@ -90,8 +175,14 @@ __global__ void __launch_bounds__(256) sc_table_kernel(const ScArgs a) {
 }
 
 cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st) {
-  dim3 grid((a.nx + 127) / 128, a.nz, a.F);
-  sc_linear_kernel<<<grid, 128, 0, st>>>(a);
+  if (!a.tiled) {
+    dim3 g2(std::min<size_t>(((size_t)a.nz * a.nx + 255) / 256, 148 * 8), a.F);
+    sc_linear_direct_kernel<<<g2, 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+  dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, a.F);
+  if (a.out_type == SUPRA_T_U8) sc_linear_tiled_kernel<true><<<grid, 256, 0, st>>>(a);
+  else sc_linear_tiled_kernel<false><<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

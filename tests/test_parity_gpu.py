@@ -221,3 +221,32 @@ def test_c2_scan_conversion_indices():
     assert np.array_equal(valid_g, valid_o)
     m = valid_o == 1
     assert np.array_equal(idx_g[m][:, [0, 2]], idx_o[m][:, [0, 2]])
+
+
+def test_c2_bench_launch_configuration():
+    """Full size, exactly the launch bench.py times: 100 frames per call (FB=8
+    frame groups incl. a ragged last group), f32 line image, u8 B-mode.
+    Sampled frames vs the oracle chain: line image <= 0.01 dB, B-mode u8
+    within 1 LSB of the oracle's u8 of its own scan conversion."""
+    w = configs.c2(sc_output_type=configs.T_U8)
+    F = 100
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    li = bf.empty_line_img(F)
+    img = bf.empty_img(F)
+    mask = bf.empty_mask()
+    bf.beamform(raw, F, line_img=li)
+    bf.scanconvert(li, F, img, mask)
+    torch.cuda.synchronize()
+    for f in (0, 57, 99):
+        raw_np = raw[f].cpu().numpy()
+        rf_o, env_o = oracle_chain(w, raw_np)
+        y_o, _ = oracle.log_compress(env_o, 50.0)
+        assert db_err(li[f].cpu().numpy(), y_o) <= DB_TOL
+        img_o, mask_o = oracle.scan_convert(w, y_o)
+        u8_o = oracle.to_u8(img_o)
+        got = img[f].cpu().numpy()
+        assert np.max(np.abs(got.astype(int) - u8_o.astype(int))) <= 1
+        if f == 0:
+            assert np.array_equal(mask.cpu().numpy(), mask_o)
+    del raw
