@@ -222,6 +222,7 @@ def main():
     import synth
     from synth import configs
     from paper_1711_06127_b200 import SupraBF
+    from paper_1711_06127_b200.dist import gather_bmode
     from paper_1711_06127_b200.pipeline import HostPipeline
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -256,7 +257,7 @@ def main():
         bf.beamform(raw, F, line_img=li)
         bf.scanconvert(li, F, img)
         if world > 1:
-            dist.gather(img, gather_list=gather, dst=0)
+            gather_bmode(img, dst=0, out=gather)
 
     for _ in range(max(3, args.warmup)):
         step()
