@@ -64,9 +64,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-__device__ __forceinline__ unsigned atom_add_shared(unsigned* p, unsigned v) {
+// acq_rel: orders this warp's reads of the slot (after __syncwarp) before the
+// count, and lets the last arriver see every other warp's release.
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
   unsigned old;
-  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v)
+               : "memory");
   return old;
 }
 
@@ -120,8 +123,16 @@ __device__ __forceinline__ float split_delay(float Ah, float B, float h, float h
 
 // int16 -> float via the 2^23 + 2^15 magic: bits (u ^ 0x4B008000) of the
 // zero-extended 16-bit value u are the float 2^23 + 2^15 + v.
-__device__ __forceinline__ float magic16(uint32_t u) { return __int_as_float((int)(u ^ 0x4B008000u)); }
-constexpr float kMagic16 = 8421376.0f;      // 2^23 + 2^15
+// int16 sample -> float: sign-extending shared load (LDS.S16) + I2FP.F32.S32
+// (the full-rate conversion; the compiler's own choice is LDS.U16 + the
+// quarter-rate I2F.S16).  `off` is a compile-time byte offset.
+__device__ __forceinline__ float lds_s16f(uint32_t addr, int off) {
+  int v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(addr + (uint32_t)off) : "memory");
+  float f;
+  asm("cvt.rn.f32.s32 %0, %1;" : "=f"(f) : "r"(v));
+  return f;
+}
 constexpr float kFloorMagic = 12582912.0f;  // 1.5 * 2^23
 constexpr int kFloorMagicBits = 0x4B400000;
 constexpr int kHalo = 64;                   // FIR halo (>= kMaxHalfTaps), each side
@@ -299,20 +310,20 @@ __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, i
     asm("mov.b32 %0, %0;" : "+r"(idx));
     float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
     w = mem ? w : 0.f;
-    const float wf = w * fr;
-    const unsigned short* px = st + idx;
+    // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
+    const float w1 = w * fr, w0 = w - w1;
+    const uint32_t pa = smem_u32(st) + 2u * (uint32_t)idx;
     if constexpr (FB == 1) {
-      const float m0 = magic16(px[0]), m1 = magic16(px[1]);
-      acc.s[m] = fmaf(w, m0 - kMagic16, acc.s[m]);
-      acc.s[m] = fmaf(wf, m1 - m0, acc.s[m]);
+      acc.s[m] = fmaf(w0, lds_s16f(pa, 0), acc.s[m]);
+      acc.s[m] = fmaf(w1, lds_s16f(pa, 2), acc.s[m]);
     } else {
 #pragma unroll
       for (int q = 0; q < FB / 2; q++) {
-        const float2 m0 = make_float2(magic16(px[(2 * q) * FR]), magic16(px[(2 * q + 1) * FR]));
-        const float2 m1 = make_float2(magic16(px[(2 * q) * FR + 1]), magic16(px[(2 * q + 1) * FR + 1]));
-        acc.p[m][q] = __ffma2_rn(make_float2(w, w), __fadd2_rn(m0, make_float2(-kMagic16, -kMagic16)),
-                                 acc.p[m][q]);
-        acc.p[m][q] = __ffma2_rn(make_float2(wf, wf), sub2(m1, m0), acc.p[m][q]);
+        // sign-extending 16-bit loads + int->float (I2FP), packed over a frame pair
+        const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
+        const float2 x1 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR + 2), lds_s16f(pa, 2 * (2 * q + 1) * FR + 2));
+        acc.p[m][q] = __ffma2_rn(make_float2(w0, w0), x0, acc.p[m][q]);
+        acc.p[m][q] = __ffma2_rn(make_float2(w1, w1), x1, acc.p[m][q]);
       }
     }
   }
@@ -382,7 +393,7 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
     mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
     tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, we.x / kRowSamples, we.y, ev, f0, &sm.full[buf]);
   };
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0 && a.debug_skip != 2)
     for (int jj = 0; jj < NS && jj < nent; jj++) produce(jj, jj);
 
   {
@@ -394,7 +405,7 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
     int buf = 0;
     unsigned phase = 0;
     for (int j = 0; j < nent; j++) {
-      mbar_wait(&sm.full[buf], phase);
+      if (a.debug_skip != 2) mbar_wait(&sm.full[buf], phase);
       const float4 r = sm.rec[j];
       const int kenter = __float_as_int(r.w);
       const int wsm = sm.wse[j].x + kFloorMagicBits - kt;
@@ -402,18 +413,17 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
       // straight-line code for the tiles at or after the entry's first
       // active tile (no per-tile branches: the chains of consecutive tiles
       // interleave)
-      dispatch_tiles<FB, NT, T0>(min(kenter / kTileK, NT - 1) / tile_gran(NT), a, r, kenter, wsm, st, kt, ktf, S,
-                                 acc);
+      if (a.debug_skip != 1)
+        dispatch_tiles<FB, NT, T0>(min(kenter / kTileK, NT - 1) / tile_gran(NT), a, r, kenter, wsm, st, kt, ktf, S,
+                                   acc);
       // release the slot; the last warp to release it refills it (no warp
       // ever waits for another to issue a copy)
       __syncwarp();
       if (lane == 0) {
-        __threadfence_block();
-        const unsigned prev = atom_add_shared(&sm.rel[buf], 1u);
+        const unsigned prev = atom_add_acqrel(&sm.rel[buf], 1u);
         if (prev == (blockDim.x / 32) - 1) {
-          __threadfence_block();
           sm.rel[buf] = 0u;
-          if (j + NS < nent) {
+          if (j + NS < nent && a.debug_skip != 2) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             produce(j + NS, buf);
           }

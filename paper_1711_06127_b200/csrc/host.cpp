@@ -282,9 +282,15 @@ supra_status build_das_tables(supra_bf* h) {
   std::vector<int32_t> nentries(G);
   std::vector<uint16_t> ncount((size_t)G * S);
   for (int g = 0; g < G; g++) {
+    // Device order: alternate the long-trace (early k_enter) and short-trace
+    // (late k_enter) ends of the sorted list, so consecutive entries in the
+    // TMA ring carry similar work and the prefetch depth in time stays even.
+    // (Sum order is fixed per configuration: results stay deterministic and
+    // identical across frames and batch sizes.)
+    const int n = (int)groups[g].size();
     for (int j = 0; j < per; j++) {
       DasEntry d{};
-      if (j < (int)groups[g].size()) d = groups[g][j];
+      if (j < n) d = groups[g][(j & 1) ? n - 1 - j / 2 : j / 2];
       else { d.kenter = 0x7fffffff; }
       flat[(size_t)g * per + j] = d;
     }
@@ -676,6 +682,8 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
   a.normalize = c.normalize;
   a.rf = rf;
   a.do_epilogue = line_img != nullptr;
+  // measurement only: 1 = TMA pipeline without the tap loop, 2 = tap loop without TMA
+  a.debug_skip = std::getenv("SUPRA_BF_DEBUG") ? std::atoi(std::getenv("SUPRA_BF_DEBUG")) : 0;
   a.fir = h->d_fir;
   a.fir_taps = c.fir_taps;
   for (int j = 0; j <= kMaxHalfTaps; j++) {

@@ -73,6 +73,7 @@ struct DasArgs {
   void* y_out;                 // [F][L][S] (fixed mode)
   int y_type;                  // SUPRA_T_F32 / SUPRA_T_U8
   unsigned* frame_max;         // [F] float bits (frame-max mode)
+  int debug_skip;              // measurement only: skip the tap loop (TMA pipeline alone)
 };
 
 struct EnvArgs {  // standalone epilogue on an RF buffer
