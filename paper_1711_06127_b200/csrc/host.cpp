@@ -77,6 +77,7 @@ struct supra_bf {
   int32_t* d_col_nl = nullptr;
   int slab_k = 2;
   int sc_tiled = 1;
+  int sc_box_k = 4, sc_box_l = 1;
   ScRow* d_rows = nullptr;
   ScEntry* d_ent = nullptr;
   // host copies for introspection
@@ -452,7 +453,9 @@ supra_status build_sc_tables(supra_bf* h) {
     }
     int maxnl = 0;
     for (int v : cnl) maxnl = std::max(maxnl, v);
-    h->sc_tiled = (maxnl <= kScMaxLines && h->slab_k <= kScMaxK) ? 1 : 0;  // else direct kernel
+    h->sc_tiled = (maxnl <= kScMaxLines && h->slab_k + 3 <= kScMaxK) ? 1 : 0;  // else direct kernel
+    h->sc_box_l = std::max(1, maxnl);
+    h->sc_box_k = std::min(kScMaxK, (h->slab_k + 3 + 3) & ~3);   // 16-byte rows, + alignment slack
     if ((e = upload(&h->d_blk_kmin, kmin)) != cudaSuccess || (e = upload(&h->d_col_l0, cl0)) != cudaSuccess ||
         (e = upload(&h->d_col_nl, cnl)) != cudaSuccess)
       return fail(SUPRA_E_RESOURCE, "sc upload: %s", cudaGetErrorString(e));
@@ -817,9 +820,16 @@ supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t fr
   a.col_l0 = h->d_col_l0;
   a.col_nl = h->d_col_nl;
   a.tiled = h->sc_tiled;
+  a.slab_box_k = h->sc_box_k;
+  a.slab_box_l = h->sc_box_l;
   a.rows = h->d_rows;
   a.ent = h->d_ent;
   a.is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
+  // bulk-copy staging of the slab: 16-byte aligned line segments
+  a.slab_tma = (c.sc_kind == SUPRA_SC_LINEAR_2D && h->sc_tiled && c.line_output_type == SUPRA_T_F32 &&
+                (h->S % 4) == 0 && ((uintptr_t)line_img & 15) == 0)
+                   ? 1
+                   : 0;
   cudaStream_t st = (cudaStream_t)stream;
   if (c.sc_kind == SUPRA_SC_LINEAR_2D) return check_launch(launch_sc_linear(a, st), "sc_linear kernel");
   return check_launch(launch_sc_table(a, st), "sc_table kernel");

@@ -140,6 +140,8 @@ struct ScArgs {
   const int32_t* col_l0;    // [ceil(nx / 256)]: first line the column tile touches
   const int32_t* col_nl;    // [ceil(nx / 256)]: lines it touches (0: none valid)
   int tiled;             // 1: tiled separable kernel; 0: direct per-pixel kernel
+  int slab_tma;          // 1: stage the slab with 1-D bulk copies (f32 line image)
+  int slab_box_k, slab_box_l;  // staged segment: samples (multiple of 4) x lines
   // table
   const ScRow* rows;     // [nz*ny]
   const ScEntry* ent;

@@ -8,6 +8,7 @@
 //   sector 2D / pyramid 3D : per output row (iz, iy) the contiguous valid x
 //               range and 16-byte entries (corner offset, fx, fy, fz).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -47,12 +48,13 @@ __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) 
 //   out[r][x] = lerp(t[r][i0], t[r][i0+1], fx(x)).
 // The slab of the line image the tile touches (lines [l0, l0+nl) x ks
 // samples from the row block's smallest k0, both host-computed) is staged in
-// shared memory with cp.async.
+// shared memory with one 1-D bulk copy (TMA) per line.
 template <bool U8OUT>
 __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
-  __shared__ float slab[kScMaxLines * kScMaxK];
+  __shared__ __align__(128) float slab[kScMaxLines * kScMaxK];
   __shared__ float tz[kScRows * kScMaxLines];
   __shared__ ScAxis saz[kScRows];
+  __shared__ __align__(8) uint64_t bar;
   const int cb = blockIdx.x, rb = blockIdx.y, f = blockIdx.z;
   const int x = cb * 256 + threadIdx.x;
   const int z0 = rb * kScRows;
@@ -63,7 +65,34 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
   const int rows = min(kScRows, a.nz - z0);
   const size_t fbase = (size_t)f * Lx * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (kmin >= 0 && nl > 0) {
+  const bool use_tma = a.in_type == SUPRA_T_F32 && a.slab_tma;
+  const int kstride = use_tma ? a.slab_box_k : ks;    // slab row stride (samples)
+  const int kal = kmin & ~3;                           // 16-byte aligned segment start
+  if (use_tma) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\nfence.mbarrier_init.release.cluster;" ::"r"(b),
+                   "r"(32)
+                   : "memory");
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // one 1-D bulk copy (TMA, UBLKCP) per line segment [kal, kal + box_k)
+      // (clipped to the record), lanes take lines
+      const float* src = (const float*)a.line_img + fbase;
+      const int seg = min(a.slab_box_k, S - kal);
+      unsigned bytes = 0;
+      for (int l = lane; l < nl && kmin >= 0; l += 32) bytes += (unsigned)seg * 4u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+      for (int l = lane; l < nl && kmin >= 0; l += 32)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(slab + l * a.slab_box_k)),
+            "l"(src + (size_t)(l0 + l) * S + kal), "r"((unsigned)seg * 4u), "r"(b)
+            : "memory");
+    }
+  }
+  if (kmin >= 0 && nl > 0 && !use_tma) {
     if (a.in_type == SUPRA_T_F32) {
       const float* src = (const float*)a.line_img + fbase;
       for (int l = warp; l < nl; l += 8)
@@ -79,8 +108,14 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
   asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
   const ScAxis ax = x < nx ? a.ax[x] : ScAxis{-1, 0.f};
   __syncthreads();
+  if (use_tma) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W_%=;\n\t}" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&bar))
+        : "memory");
+  }
   if ((int)threadIdx.x < nl) {
-    const float* y = slab + threadIdx.x * ks - kmin;
+    const float* y = slab + threadIdx.x * kstride - (use_tma ? kal : kmin);
     for (int r = 0; r < rows; r++) {
       const ScAxis az = saz[r];
       if (az.i0 >= 0) tz[r * kScMaxLines + threadIdx.x] = fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]);
