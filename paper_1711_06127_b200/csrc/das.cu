@@ -248,7 +248,7 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
       const size_t out = ((size_t)f * a.L + line) * a.S + k;
       if (a.ref_fixed) {
         const float e = env[q];
-        const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, log2f(e), a.log_k0), 0.f), 1.f) : 0.f;
+        const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(e), a.log_k0), 0.f), 1.f) : 0.f;
         if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[out] = (uint8_t)floorf(255.f * y + 0.5f);
         else ((float*)a.y_out)[out] = y;
       } else {

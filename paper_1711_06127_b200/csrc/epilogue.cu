@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
     const float env = envelope_at(rfs + P + k, cs, cs + kMaxHalfTaps + 1, P);
     const size_t o = ((size_t)f * a.L + line) * S + k;
     if (a.ref_fixed) {
-      const float y = env > 0.f ? fminf(fmaxf(fmaf(a.log_k1, log2f(env), a.log_k0), 0.f), 1.f) : 0.f;
+      const float y = env > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(env), a.log_k0), 0.f), 1.f) : 0.f;
       if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[o] = (uint8_t)floorf(255.f * y + 0.5f);
       else ((float*)a.y_out)[o] = y;
     } else {
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
     const long long e0 = vec ? i * 4 : i;
     const int f = (int)(e0 / per);
     const float ref = __uint_as_float(a.frame_max[f]);
-    const float lref = ref > 0.f ? log2f(ref) : 0.f;
+    const float lref = ref > 0.f ? lg2_approx(ref) : 0.f;
     float v[4];
     int n = vec ? 4 : 1;
     if (vec) {
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
     for (int j = 0; j < 4; j++) {
       if (j < n) {
         float e = v[j];
-        y[j] = (e > 0.f && ref > 0.f) ? fminf(fmaxf(fmaf(a.DR_k, log2f(e) - lref, 1.f), 0.f), 1.f) : 0.f;
+        y[j] = (e > 0.f && ref > 0.f) ? fminf(fmaxf(fmaf(a.DR_k, lg2_approx(e) - lref, 1.f), 0.f), 1.f) : 0.f;
       }
     }
     if (a.y_type == SUPRA_T_U8) {

@@ -52,7 +52,7 @@ __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) 
 template <bool U8OUT>
 __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
   __shared__ __align__(128) float slab[kScMaxLines * kScMaxK];
-  __shared__ float tz[kScRows * kScMaxLines];
+  __shared__ float tz[kScRows * (kScMaxLines + 2)];
   __shared__ ScAxis saz[kScRows];
   __shared__ __align__(8) uint64_t bar;
   const int cb = blockIdx.x, rb = blockIdx.y, f = blockIdx.z;
@@ -114,34 +114,37 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
             (uint32_t)__cvta_generic_to_shared(&bar))
         : "memory");
   }
+  // depth lerp t[r][l]; rows without a valid k0 and the spare pair of
+  // columns [kScMaxLines, kScMaxLines+1] are zero, so the pixel loop below
+  // needs no predicates (invalid columns read the zero pair with fx = 0)
+  constexpr int TZS = kScMaxLines + 2;
   if ((int)threadIdx.x < nl) {
     const float* y = slab + threadIdx.x * kstride - (use_tma ? kal : kmin);
     for (int r = 0; r < rows; r++) {
       const ScAxis az = saz[r];
-      if (az.i0 >= 0) tz[r * kScMaxLines + threadIdx.x] = fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]);
+      tz[r * TZS + threadIdx.x] = az.i0 >= 0 ? fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]) : 0.f;
     }
   }
+  if (threadIdx.x < 2 * kScRows) tz[(threadIdx.x >> 1) * TZS + kScMaxLines + (threadIdx.x & 1)] = 0.f;
   __syncthreads();
   if (x >= nx) return;
   const bool colok = ax.i0 >= 0;
-  const float* tcol = tz + (colok ? ax.i0 - l0 : 0);
+  const float* tcol = tz + (colok ? ax.i0 - l0 : kScMaxLines);
+  const float fx = colok ? ax.f : 0.f;
   const size_t out0 = ((size_t)f * a.nz + z0) * nx + x;
   if (U8OUT) {
     uint8_t* o = (uint8_t*)a.img + out0;
-#pragma unroll 4
+#pragma unroll 8
     for (int r = 0; r < rows; r++, o += nx) {
-      const bool ok = colok && saz[r].i0 >= 0;
-      const float t0 = tcol[r * kScMaxLines], t1 = tcol[r * kScMaxLines + 1];
-      const float v = ok ? fmaf(ax.f, t1 - t0, t0) : 0.f;
-      *o = (uint8_t)floorf(fmaf(255.f, v, 0.5f));
+      const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
+      *o = (uint8_t)floorf(fmaf(255.f, fmaf(fx, t1 - t0, t0), 0.5f));
     }
   } else {
     float* o = (float*)a.img + out0;
-#pragma unroll 4
+#pragma unroll 8
     for (int r = 0; r < rows; r++, o += nx) {
-      const bool ok = colok && saz[r].i0 >= 0;
-      const float t0 = tcol[r * kScMaxLines], t1 = tcol[r * kScMaxLines + 1];
-      *o = ok ? fmaf(ax.f, t1 - t0, t0) : 0.f;
+      const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
+      *o = fmaf(fx, t1 - t0, t0);
     }
   }
   if (a.mask && f == 0)
