@@ -333,8 +333,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, cores, sample = oracle_frame_rate(w, raw[0].cpu().numpy(), 20.0)
         cpu_baseline = {"value": r, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample}
-    if rank == 0 and world == 1 and not args.no_secondary:
-        secondary = secondary_3d(local)
+    if not args.no_secondary:
+        secondary = secondary_3d(local, world, rank)
 
     if rank == 0:
         line = {
@@ -357,38 +357,74 @@ def main():
     return 0
 
 
-def secondary_3d(dev_index: int):
+def secondary_3d(dev_index: int, world: int = 1, rank: int = 0, vols: int = 8):
     """Volumes/s on C4b (3D 32x32 matrix probe, 64x64 lines, 4x4 multi-line,
-    pyramid scan conversion to 256^3), device-timed -- the metric's 3D half."""
+    pyramid scan conversion to 256^3, u8 line image and volume):
+      * "C4b_stream": ``vols`` volumes per call on every rank (C5's batched 3D
+        stream; one 1 GiB volume synthesised and replicated -- DAS cost is
+        data-independent), value = all ranks' volumes / max-over-ranks time;
+      * "C4b_single": ONE volume per call, latency mode: the
+        scanlines are split into event-aligned blocks over the ranks
+        (dist.ShardedVolume: DAS+envelope per block, all-reduce(max) of the
+        frame max, log compression, NCCL all-gather of the u8 line volume),
+        rank 0 scan-converts.  At N=1 it is the plain single-GPU call.
+    Device-timed with CUDA events, inputs resident in HBM (> L2)."""
     import torch
+    import torch.distributed as dist
     import synth
     from synth import configs
     from paper_1711_06127_b200 import SupraBF
+    from paper_1711_06127_b200.dist import ShardedVolume
     out = {}
-    for name in ("C4b",):
-        w = configs.CONFIGS[name]().replace(sc_output_type=configs.T_U8)
-        raw = torch.empty((1, w.num_events, w.C, w.S), dtype=torch.int16, device=f"cuda:{dev_index}")
-        synth.channel_data_gpu(w, raw[0], realisation=0)
-        bf = SupraBF(w, device=dev_index, max_frames=1)
-        li, img = bf.empty_line_img(1), bf.empty_img(1)
-        for _ in range(3):
-            bf.beamform(raw, 1, line_img=li)
-            bf.scanconvert(li, 1, img)
+    w = configs.CONFIGS["C4b"]().replace(sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
+    dev = torch.device(f"cuda:{dev_index}")
+    raw = torch.empty((vols, w.num_events, w.C, w.S), dtype=torch.int16, device=dev)
+    synth.channel_data_gpu(w, raw[0], realisation=0)
+    for v in range(1, vols):
+        raw[v].copy_(raw[0])
+    bf = SupraBF(w, device=dev_index, max_frames=vols)
+    li, img = bf.empty_line_img(vols), bf.empty_img(vols)
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 20
         a.record()
-        for _ in range(n):
-            bf.beamform(raw, 1, line_img=li)
-            bf.scanconvert(li, 1, img)
+        for _ in range(reps):
+            fn()
         b.record()
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / n
-        out[name] = {"value": 1000.0 / ms, "unit": "volumes/s", "ms_per_volume": ms,
-                     "note": "device-timed, input resident; 1 GiB/volume < L2? no (1 GiB > 126 MB)"}
-        bf.close()
-        del raw
-        torch.cuda.empty_cache()
+        t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    def stream_call():
+        bf.beamform(raw, vols, line_img=li)
+        bf.scanconvert(li, vols, img)
+
+    ms = timed(stream_call, 5)
+    out["C4b_stream"] = {"value": vols * world * 1000.0 / ms, "unit": "volumes/s", "ms_per_call": ms,
+                         "volumes_per_call_per_rank": vols, "scaling": "weak"}
+
+    sv = ShardedVolume(bf, w.L, w.S, torch.uint8, dev, align=4 * w.num_lines_x)
+
+    def single_call():
+        y = sv.run(raw[:1])
+        if rank == 0:
+            bf.scanconvert(y, 1, img)
+
+    ms = timed(single_call, 10)
+    out["C4b_single"] = {"value": 1000.0 / ms, "unit": "volumes/s", "ms_per_volume": ms,
+                         "volumes_per_call": 1, "scaling": "strong",
+                         "parallelism": f"scanline blocks x{world}, all-reduce(max) + all-gather u8 line volume"
+                         if world > 1 else "single GPU"}
+    bf.close()
+    del raw, li, img, sv
+    torch.cuda.empty_cache()
     return out
 
 

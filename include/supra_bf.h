@@ -167,6 +167,39 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float *rf, int32_t frames
                                    void *stream);
 
 /*
+ * Split form of supra_bf_beamform for one volume sharded over GPUs by
+ * scanline blocks (latency mode; each transmit event's data
+ * is read only by its own lines, so a contiguous line range reads a
+ * disjoint part of the input when event blocks align with the range).
+ *
+ * supra_bf_beamform_lines -- DAS + IQ envelope (the formulas of
+ * supra_bf_beamform, without the log step) for lines
+ * [line_first, line_first + line_count) of every frame.
+ *   env       : device float [frames][L][samples]; only the range's rows are
+ *               written (envelope, >= 0).
+ *   frame_max : device float [frames]; receives the maximum of env over the
+ *               range (0 for an all-zero range) -- all-reduce(max) it across
+ *               ranks to get the frame-max reference of S:267.
+ * Errors: SUPRA_E_STRUCT on NULL, a range outside [0, L), frames out of
+ * range, raw misaligned, or a pointer that is not device memory.
+ *
+ * supra_bf_log_compress -- y = clamp((20 log10(env/ref) + DR)/DR, 0, 1)
+ * (0 where env = 0 or ref = 0) on the same line range; ref =
+ * frame_max[f] (device float [frames]) in SUPRA_REF_FRAME_MAX mode,
+ * reference_value in SUPRA_REF_FIXED mode (frame_max may then be NULL).
+ *   line_img  : device [frames][L][samples] of line_output_type; only the
+ *               range's rows are written.  env and line_img may alias only
+ *               when line_output_type is SUPRA_T_F32 (element-wise, in place).
+ * Errors: SUPRA_E_STRUCT on NULL (frame_max NULL in FRAME_MAX mode), a range
+ * outside [0, L), frames out of range.
+ */
+supra_status supra_bf_beamform_lines(supra_bf_t h, const void *raw, int32_t frames, int32_t line_first,
+                                     int32_t line_count, float *env, float *frame_max, void *stream);
+supra_status supra_bf_log_compress(supra_bf_t h, const float *env, int32_t frames, int32_t line_first,
+                                   int32_t line_count, const float *frame_max, void *line_img,
+                                   void *stream);
+
+/*
  * supra_bf_scanconvert -- scan conversion in 2D and 3D (S:285-
  * 311): per output pixel/voxel the create-time table gives validity, integer
  * indices (built in binary64, bit-exact with the analytic inverse map) and

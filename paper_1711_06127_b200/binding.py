@@ -26,7 +26,7 @@ SC_LINEAR_2D, SC_SECTOR_2D, SC_PYRAMID_3D = 0, 1, 2
 
 EXPORTS = ("supra_bf_create", "supra_bf_beamform", "supra_bf_envelope_log", "supra_bf_scanconvert",
            "supra_bf_destroy", "supra_bf_last_error", "supra_bf_sc_indices", "supra_bf_info",
-           "supra_bf_set_das_events")
+           "supra_bf_set_das_events", "supra_bf_beamform_lines", "supra_bf_log_compress")
 
 
 class SupraError(RuntimeError):
@@ -92,6 +92,10 @@ def lib():
         L.supra_bf_info.restype = C.c_int
         L.supra_bf_set_das_events.argtypes = [vp, vp, vp]
         L.supra_bf_set_das_events.restype = C.c_int
+        L.supra_bf_beamform_lines.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]
+        L.supra_bf_beamform_lines.restype = C.c_int
+        L.supra_bf_log_compress.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]
+        L.supra_bf_log_compress.restype = C.c_int
         _lib = L
     return _lib
 
@@ -169,6 +173,18 @@ class SupraBF:
     def envelope_log(self, rf, frames: int, line_img, stream=None):
         _check(lib().supra_bf_envelope_log(self.h, _ptr(rf), frames, _ptr(line_img),
                                            _stream(stream)))
+
+    def beamform_lines(self, raw, frames: int, line_first: int, line_count: int, env, frame_max,
+                       stream=None):
+        """DAS + envelope for a line range; env f32 [F][L][S], frame_max f32 [F]."""
+        _check(lib().supra_bf_beamform_lines(self.h, _ptr(raw), frames, line_first, line_count,
+                                             _ptr(env), _ptr(frame_max), _stream(stream)))
+
+    def log_compress(self, env, frames: int, line_first: int, line_count: int, frame_max, line_img,
+                     stream=None):
+        """Log compression of a line range against frame_max (or the fixed reference)."""
+        _check(lib().supra_bf_log_compress(self.h, _ptr(env), frames, line_first, line_count,
+                                           _ptr(frame_max), _ptr(line_img), _stream(stream)))
 
     def scanconvert(self, line_img, frames: int, img, mask=None, stream=None):
         _check(lib().supra_bf_scanconvert(self.h, _ptr(line_img), frames, _ptr(img), _ptr(mask),

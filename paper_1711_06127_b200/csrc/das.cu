@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
   constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
   const size_t SB = stage_bytes(FB, NT * 8 + 2);
   SmemLayout sm = carve(smem_raw, FB, S, a.entries_per_group);
-  const int line = blockIdx.x;
+  const int line = a.line0 + blockIdx.x;
   const int f0 = blockIdx.y * FB;
   const int g = a.line_group[line];
   const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
@@ -526,7 +526,7 @@ static cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_
   auto kern = das_fused_kernel<FB, NT, T0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(a.L, (a.F + FB - 1) / FB);
+  dim3 grid(a.nlines, (a.F + FB - 1) / FB);
   kern<<<grid, 256, smem, st>>>(tm, a);
   return cudaGetLastError();
 }

@@ -50,24 +50,27 @@ __global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
 
 // y = 1 + (20 log10 2 / DR) (log2 env - log2 ref), clamped to [0,1]; env = 0
 // or an all-zero frame -> 0.  Grid-stride, 4 samples/thread.
+// Element e0 of the converted set lives at f * frame_stride + offset + (e0 - f * per)
+// in both env and y (a contiguous line range of each frame).
 __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
   const long long per = a.per_frame;
   const long long total = per * a.F;
   const long long n4 = total >> 2;
-  const bool vec = (per & 3) == 0;
+  const bool vec = ((per | a.frame_stride | a.offset) & 3) == 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (vec ? n4 : total); i += stride) {
     const long long e0 = vec ? i * 4 : i;
     const int f = (int)(e0 / per);
-    const float ref = __uint_as_float(a.frame_max[f]);
+    const long long ad = e0 + (long long)f * (a.frame_stride - per) + a.offset;
+    const float ref = a.frame_max ? __uint_as_float(a.frame_max[f]) : a.fixed_ref;
     const float lref = ref > 0.f ? lg2_approx(ref) : 0.f;
     float v[4];
     int n = vec ? 4 : 1;
     if (vec) {
-      float4 x = reinterpret_cast<const float4*>(a.env)[i];
+      float4 x = *reinterpret_cast<const float4*>(a.env + ad);
       v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
     } else {
-      v[0] = a.env[e0];
+      v[0] = a.env[ad];
     }
     float y[4];
 #pragma unroll
@@ -85,14 +88,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
         q.y = (uint8_t)floorf(255.f * y[1] + 0.5f);
         q.z = (uint8_t)floorf(255.f * y[2] + 0.5f);
         q.w = (uint8_t)floorf(255.f * y[3] + 0.5f);
-        reinterpret_cast<uchar4*>(o)[i] = q;
+        *reinterpret_cast<uchar4*>(o + ad) = q;
       } else {
-        o[e0] = (uint8_t)floorf(255.f * y[0] + 0.5f);
+        o[ad] = (uint8_t)floorf(255.f * y[0] + 0.5f);
       }
     } else {
       float* o = (float*)a.y_out;
-      if (vec) reinterpret_cast<float4*>(o)[i] = make_float4(y[0], y[1], y[2], y[3]);
-      else o[e0] = y[0];
+      if (vec) *reinterpret_cast<float4*>(o + ad) = make_float4(y[0], y[1], y[2], y[3]);
+      else o[ad] = y[0];
     }
   }
 }
@@ -109,7 +112,7 @@ cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st) {
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
   long long total = a.per_frame * a.F;
-  long long work = (a.per_frame & 3) == 0 ? total / 4 : total;
+  long long work = ((a.per_frame | a.frame_stride | a.offset) & 3) == 0 ? total / 4 : total;
   int blocks = (int)std::min<long long>((work + 255) / 256, 148LL * 16);
   if (blocks < 1) blocks = 1;
   finalize_kernel<<<blocks, 256, 0, st>>>(a);

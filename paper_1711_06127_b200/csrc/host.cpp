@@ -660,10 +660,14 @@ supra_status supra_bf_info(supra_bf_t h, int64_t* info8) {
   return SUPRA_OK;
 }
 
-static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float* rf, void* line_img,
-                            cudaStream_t st) {
+// env_ext != NULL: envelope-only mode for a line range (supra_bf_beamform_lines):
+// the envelope goes to env_ext, per-frame maxima to fmax_ext, no log pass.
+static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int line0, int nlines, float* rf,
+                            void* line_img, float* env_ext, float* fmax_ext, cudaStream_t st) {
   const supra_bf_config& c = h->cfg;
   DasArgs a{};
+  a.line0 = line0;
+  a.nlines = nlines;
   a.raw = (const int16_t*)raw;
   a.F = frames;
   a.E = h->E;
@@ -695,7 +699,14 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
   }
   fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
   a.y_type = c.line_output_type;
-  if (line_img) {
+  if (env_ext) {
+    a.do_epilogue = 1;
+    a.ref_fixed = 0;
+    a.env_out = env_ext;
+    a.frame_max = (unsigned*)fmax_ext;  // non-negative floats: bit order = value order
+    cudaError_t e = cudaMemsetAsync(fmax_ext, 0, sizeof(float) * frames, st);
+    if (e != cudaSuccess) return check_launch(e, "memset frame_max");
+  } else if (line_img) {
     if (a.ref_fixed) {
       a.y_out = line_img;
     } else {
@@ -712,10 +723,11 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, float
   if (h->ev_before) cudaEventRecord(h->ev_before, st);
   supra_status s = check_launch(launch_das(tm, a, fb, st), "das kernel");
   if (h->ev_after) cudaEventRecord(h->ev_after, st);
-  if (s != SUPRA_OK || !line_img || a.ref_fixed) return s;
+  if (s != SUPRA_OK || !line_img || a.ref_fixed || env_ext) return s;
   FinalizeArgs fa{};
   fa.env = a.env_out;
   fa.per_frame = (long long)h->L * h->S;
+  fa.frame_stride = fa.per_frame;
   fa.F = frames;
   fa.frame_max = h->d_frame_max;
   fa.DR_k = a.log_k1;
@@ -741,7 +753,70 @@ supra_status supra_bf_beamform(supra_bf_t h, const void* raw, int32_t frames, fl
     return fail(SUPRA_E_STRUCT, "line_img is not device memory of device %d", dev);
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return fail(SUPRA_E_CUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
-  return run_das(h, raw, frames, rf, line_img, (cudaStream_t)stream);
+  return run_das(h, raw, frames, 0, h->L, rf, line_img, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+supra_status supra_bf_beamform_lines(supra_bf_t h, const void* raw, int32_t frames, int32_t line_first,
+                                     int32_t line_count, float* env, float* frame_max, void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (line_first < 0 || line_count < 0 || line_first + (int64_t)line_count > h->L)
+    return fail(SUPRA_E_STRUCT, "line range [%d, %d + %d) outside [0, %d)", line_first, line_first, line_count,
+                h->L);
+  if (!env || !frame_max) return fail(SUPRA_E_STRUCT, "env and frame_max must not be NULL");
+  if (frames == 0 || line_count == 0) {
+    if (frames > 0) {
+      DeviceGuard dg(h->cfg.device);
+      return check_launch(cudaMemsetAsync(frame_max, 0, sizeof(float) * frames, (cudaStream_t)stream),
+                          "memset frame_max");
+    }
+    return SUPRA_OK;
+  }
+  if (!raw || ((uintptr_t)raw & 15)) return fail(SUPRA_E_STRUCT, "raw must be a 16-byte aligned device pointer");
+  DeviceGuard dg(h->cfg.device);
+  const int dev = h->cfg.device;
+  if (!is_device_ptr(raw, dev) || !is_device_ptr(env, dev) || !is_device_ptr(frame_max, dev))
+    return fail(SUPRA_E_STRUCT, "raw / env / frame_max are not device memory of device %d", dev);
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return fail(SUPRA_E_CUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
+  return run_das(h, raw, frames, line_first, line_count, nullptr, nullptr, env, frame_max, (cudaStream_t)stream);
+}
+
+supra_status supra_bf_log_compress(supra_bf_t h, const float* env, int32_t frames, int32_t line_first,
+                                   int32_t line_count, const float* frame_max, void* line_img, void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (line_first < 0 || line_count < 0 || line_first + (int64_t)line_count > h->L)
+    return fail(SUPRA_E_STRUCT, "line range [%d, %d + %d) outside [0, %d)", line_first, line_first, line_count,
+                h->L);
+  if (!env || !line_img) return fail(SUPRA_E_STRUCT, "env and line_img must not be NULL");
+  const supra_bf_config& c = h->cfg;
+  if (!frame_max && c.reference_mode != SUPRA_REF_FIXED)
+    return fail(SUPRA_E_STRUCT, "frame_max is NULL but reference_mode is FRAME_MAX");
+  if (frames == 0 || line_count == 0) return SUPRA_OK;
+  DeviceGuard dg(c.device);
+  const int dev = c.device;
+  if (!is_device_ptr(env, dev) || !is_device_ptr(line_img, dev) || (frame_max && !is_device_ptr(frame_max, dev)))
+    return fail(SUPRA_E_STRUCT, "env / frame_max / line_img are not device memory of device %d", dev);
+  int fixed;
+  float k1, k0;
+  fill_log(h, fixed, k1, k0);
+  FinalizeArgs fa{};
+  fa.env = env;
+  fa.per_frame = (long long)line_count * h->S;
+  fa.frame_stride = (long long)h->L * h->S;
+  fa.offset = (long long)line_first * h->S;
+  fa.F = frames;
+  fa.frame_max = fixed ? nullptr : (const unsigned*)frame_max;
+  fa.fixed_ref = (float)c.reference_value;
+  fa.DR_k = k1;
+  fa.y_out = line_img;
+  fa.y_type = c.line_output_type;
+  return check_launch(launch_finalize(fa, (cudaStream_t)stream), "log kernel");
 }
 
 supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames, void* line_img, void* stream) {
@@ -779,6 +854,7 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames
   FinalizeArgs fa{};
   fa.env = a.env_out;
   fa.per_frame = (long long)h->L * h->S;
+  fa.frame_stride = fa.per_frame;
   fa.F = frames;
   fa.frame_max = h->d_frame_max;
   fa.DR_k = a.log_k1;

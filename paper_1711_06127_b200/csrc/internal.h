@@ -47,6 +47,7 @@ struct DasArgs {
   int ntiles;              // ceil(S / kTileK)
   int entries_per_group;   // row stride of `entries`
   int rows;                // trace rows per TMA box: S / kRowSamples + 2
+  int line0, nlines;           // lines [line0, line0 + nlines) of every frame are beamformed
   const int32_t* line_group;   // [L]
   const DasEntry* entries;     // [G][entries_per_group], sorted by kenter
   const int32_t* nentries;     // [G]: entries with kenter < S
@@ -89,11 +90,13 @@ struct EnvArgs {  // standalone epilogue on an RF buffer
   unsigned* frame_max;
 };
 
-struct FinalizeArgs {  // frame-max reference: env -> y
-  const float* env;    // [F][L*S]
-  long long per_frame; // L*S
+struct FinalizeArgs {  // env -> y with a per-frame (or fixed) reference
+  const float* env;    // [F][frame_stride], elements [offset, offset + per_frame) of each frame
+  long long per_frame; // elements converted per frame (L*S, or nlines*S for a line range)
+  long long frame_stride, offset;
   int F;
-  const unsigned* frame_max;
+  const unsigned* frame_max;  // [F] float bits of the reference; NULL -> fixed_ref
+  float fixed_ref;
   float DR_k;          // 20 log10(2) / DR
   void* y_out;
   int y_type;

@@ -43,3 +43,68 @@ def frame_max_allreduce(frame_max: torch.Tensor) -> torch.Tensor:
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(frame_max, op=dist.ReduceOp.MAX)
     return frame_max
+
+
+def shard_lines(L: int, world: int, rank: int, align: int = 1) -> Tuple[int, int]:
+    """Contiguous block of scanlines for ``rank``: (first, count), block
+    boundaries on multiples of ``align`` lines (align = lines per event block,
+    so each transmit event's data is read by exactly one rank).
+    Covers [0, L) exactly once; requires L % align == 0."""
+    if L % align:
+        raise ValueError(f"L={L} is not a multiple of align={align}")
+    first, n = shard_frames(L // align, world, rank)
+    return first * align, n * align
+
+
+class ShardedVolume:
+    """Latency mode: ONE volume beamformed by all ranks, each
+    on a contiguous scanline block.  Per call:
+      1. DAS + envelope of the rank's lines (supra_bf_beamform_lines),
+      2. all-reduce(max) of the frame maximum (the log reference of S:267;
+         skipped for a fixed reference),
+      3. log compression of the rank's lines against the global maximum,
+      4. all-gather of the line-domain slabs so every rank holds the volume
+         (u8 for C4: 8 MiB in total) -- the scan conversion then runs on
+         rank 0 (or on any rank) from the full line image.
+    No input exchange: the blocks read disjoint events.  ``bf`` is a SupraBF
+    handle (or any object with beamform_lines / log_compress of the same
+    signature); ``y_dtype`` is the line-image dtype of its config."""
+
+    def __init__(self, bf, L: int, S: int, y_dtype: torch.dtype, device, align: int = 1,
+                 fixed_reference: bool = False):
+        self.bf = bf
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.L, self.S = L, S
+        self.first, self.count = shard_lines(L, self.world, self.rank, align)
+        self.ranges = [shard_lines(L, self.world, r, align) for r in range(self.world)]
+        counts = [c for _, c in self.ranges]
+        self.chunk = max(counts)
+        self.equal = all(c == self.chunk for c in counts)
+        self.fixed = fixed_reference
+        self.env = torch.empty((1, L, S), dtype=torch.float32, device=device)
+        self.fmax = torch.zeros((1,), dtype=torch.float32, device=device)
+        self.y = torch.zeros((1, L, S), dtype=y_dtype, device=device)
+        self.send = torch.zeros((self.chunk, S), dtype=y_dtype, device=device)
+        if not self.equal:
+            self.recv = torch.zeros((self.world, self.chunk, S), dtype=y_dtype, device=device)
+
+    def run(self, raw, stream=None) -> torch.Tensor:
+        """Beamform one volume (raw [1][E][C][S] on this rank's device; only
+        this rank's events are read) -> full line image [1][L][S] on every rank."""
+        a, n = self.first, self.count
+        self.bf.beamform_lines(raw, 1, a, n, self.env, self.fmax, stream)
+        if not self.fixed:
+            frame_max_allreduce(self.fmax)
+        self.bf.log_compress(self.env, 1, a, n, self.fmax, self.y, stream)
+        if self.world == 1:
+            return self.y
+        flat = self.y.view(self.L, self.S)
+        self.send[:n].copy_(flat[a:a + n])
+        if self.equal:       # rank r's block is rows [r*chunk, (r+1)*chunk): gather straight into y
+            dist.all_gather_into_tensor(flat, self.send)
+        else:
+            dist.all_gather_into_tensor(self.recv.view(self.world * self.chunk, self.S), self.send)
+            for r, (f, c) in enumerate(self.ranges):
+                flat[f:f + c].copy_(self.recv[r, :c])
+        return self.y

@@ -71,3 +71,80 @@ def test_gather_and_allreduce_gloo_world2():
         assert torch.all(allf[f] == f)
     for r in range(world):
         assert res[r][1] == [2.0, 0.5]
+
+
+@pytest.mark.parametrize("L,world,align", [(4096, 8, 256), (4096, 2, 256), (192, 4, 1), (10, 3, 2), (8, 1, 4)])
+def test_shard_lines_partition(L, world, align):
+    from paper_1711_06127_b200.dist import shard_lines
+    seen = []
+    for r in range(world):
+        first, n = shard_lines(L, world, r, align)
+        assert first % align == 0 and n % align == 0
+        seen.extend(range(first, first + n))
+    assert seen == list(range(L))
+
+
+def test_c4b_line_blocks_read_disjoint_events():
+    """With 4-row alignment (256 lines) every transmit event of C4b is read
+    by exactly one rank: the latency-mode input needs no exchange."""
+    from synth import configs
+    from paper_1711_06127_b200.dist import shard_lines
+    w = configs.c4("b")
+    for world in (2, 4, 8):
+        owners = {}
+        for r in range(world):
+            a, n = shard_lines(w.L, world, r, 4 * w.num_lines_x)
+            for e in set(w.line_event[a:a + n].tolist()):
+                assert owners.setdefault(e, r) == r
+        assert len(owners) == w.num_events
+
+
+class _StubBF:
+    """CPU stand-in with the SupraBF line-range signatures: env[l][k] =
+    (l + 1) * (k + 1) (max over a range is at its last line, last sample);
+    log_compress writes env / frame_max."""
+
+    def beamform_lines(self, raw, frames, first, count, env, fmax, stream=None):
+        S = env.shape[-1]
+        l = torch.arange(first, first + count, dtype=torch.float32)[:, None]
+        k = torch.arange(S, dtype=torch.float32)[None]
+        env[0, first:first + count] = (l + 1) * (k + 1)
+        fmax[0] = env[0, first:first + count].max() if count else 0.0
+
+    def log_compress(self, env, frames, first, count, fmax, y, stream=None):
+        y[0, first:first + count] = env[0, first:first + count] / fmax[0]
+
+
+def _vol_worker(rank, world, port, L, align, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1711_06127_b200.dist import ShardedVolume
+        sv = ShardedVolume(_StubBF(), L, 8, torch.float32, "cpu", align=align)
+        y = sv.run(None)
+        q.put((rank, y.clone().numpy(), float(sv.fmax[0])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,align", [(16, 4), (12, 1)])   # equal blocks / unequal blocks (5, 4, ... )
+def test_sharded_volume_gloo_world2(L, align):
+    world = 2 if L == 16 else 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vol_worker, args=(r, world, port, L, align, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (y, m)) for r, y, m in (q.get(timeout=120) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    S = 8
+    full = (torch.arange(L, dtype=torch.float64)[:, None] + 1) * (torch.arange(S, dtype=torch.float64)[None] + 1)
+    expect = (full / full.max()).numpy()
+    for r in range(world):
+        y, m = res[r]
+        assert m == float(L * S)                       # the global frame max on every rank
+        assert abs(y[0] - expect).max() < 1e-6         # every rank holds the whole line image
