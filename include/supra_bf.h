@@ -236,8 +236,9 @@ supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t *valid, int32_t *idx);
 
 /*
  * supra_bf_info -- launch facts for the bench (host int64 [8]):
- *   [0] kernels launched per beamform call with line_img (DAS + finalize),
- *   [1] DAS frames batched per CTA, [2] DAS depth tile, [3] referenced input
+ *   [0] kernels launched per beamform call with line_img at max_frames_per_call
+ *   (DAS, + a second DAS launch for frames % [1], + finalize in frame-max mode),
+ *   [1] DAS frames batched per CTA, [2] DAS depth samples per pass, [3] referenced input
  *   bytes per frame (distinct int16 samples any tap reads x 2),
  *   [4] taps per frame, [5] scan-conversion table bytes, [6] valid output
  *   pixels, [7] kernels per scanconvert call.

@@ -2,29 +2,31 @@
 // IQ-envelope / log-compression epilogue (
 // S:133).
 //
-// One CTA = one scanline x FB frames.  The loop runs over the line's receive
-// aperture entries (channels, pre-sorted by aperture entry depth k_enter in
-// binary64, reading #6); every consumer thread keeps the RF of its NT output
-// samples k = kt + 256 m for all FB frames in registers.  Warp-specialised:
-//   warp 8 (producer): per entry ONE 5-D TMA (cp.async.bulk.tensor -> SASS
-//     UTMALDG) fetches the entry's whole referenced trace [ws, S) for the FB
-//     frames into a 3-stage shared-memory ring -- each referenced sample is
-//     read from HBM once, the start is 32-sample aligned, samples < 0 or
-//     >= S come back as zeros (the TMA out-of-bounds fill = the zero
-//     padding of reading #10).  It also publishes the entry record
-//     {|q|^2/2, d.q, pi cu, k_enter} so consumers do no dot products.
-//   warps 0-7 (consumers): per entry and output tile, the closed-form split
-//     delay tau = k + delta, delta = |q + h d| - h (h = k/2 in sample units)
-//     with one MUFU.RSQ + Newton correction (reading #30), magic-number
-//     floor, Hann weight (MUFU.COS), then for each frame pair the int16->f32
-//     magic conversion, linear interpolation and accumulation in packed
-//     f32x2 (FADD2/FFMA2): geometry is amortised over the FB frames.
-// After the last entry RF = sum / N (N from a binary64-derived count table)
-// is written to shared memory (reusing the trace ring) in a padded,
-// bank-conflict-free layout and the epilogue runs the 65-tap complex FIR as
-// a sliding window (4 outputs x 4 frames per thread, taps in the constant
-// bank), |.|, then 20 log10 against a fixed reference, or env + per-frame
-// max for the frame-max reference (finalised by finalize_kernel).
+// One CTA = one scanline x FB frames (256 threads, 2 CTAs per SM).  Depth is
+// processed in passes of PL = 256 NT samples; in a pass every thread keeps
+// the RF of its NT output samples k = k0 + kt + 256 m for all FB frames in
+// registers (FB x NT = 64 accumulators, packed f32x2).  Per pass the loop
+// runs over the line's receive-aperture entries (channels sorted by
+// aperture entry depth k_enter in binary64, reading #6) that are members
+// somewhere in the pass:
+//   * per entry ONE 5-D TMA (cp.async.bulk.tensor -> SASS UTMALDG) fetches
+//     the entry's referenced trace window for the pass, for all FB frames,
+//     into a shared-memory ring; samples < 0 or >= S come back as zeros
+//     (the TMA out-of-bounds fill = the zero padding of reading #10).  The
+//     last warp to release a ring slot refills it -- no producer warp.
+//   * per entry and output tile: the closed-form split delay tau = k + delta,
+//     delta = |q + h d| - h (h = k/2 in sample units) with one MUFU.RSQ +
+//     Newton correction (reading #30), magic-number floor, Hann weight
+//     (MUFU.COS), then per frame pair two sign-extending LDS.S16 + I2FP and
+//     the interpolating accumulation in FFMA2: the geometry is amortised
+//     over the FB frames.
+// After a pass RF = sum / N (N from a binary64-derived count table) goes to
+// a padded shared-memory line buffer (aliasing the drained ring) and the
+// 65-tap complex FIR runs over the outputs whose taps are complete, as a
+// sliding window (4 outputs x 4 frames per thread, taps in the constant
+// bank); the last 2P RF samples carry over to the next pass.  |.|, then
+// 20 log10 against a fixed reference, or env + per-frame max for the
+// frame-max reference (finalised by finalize_kernel).
 #include "internal.h"
 
 namespace supra {
@@ -37,12 +39,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
-      : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
@@ -58,9 +54,9 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
+      "r"(parity)
       : "memory");
 }
 
@@ -82,9 +78,6 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
 }
-
-// Named barrier over the 256 consumer threads (warps 0-7) only.
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
@@ -121,8 +114,6 @@ __device__ __forceinline__ float split_delay(float Ah, float B, float h, float h
   return fmaf(y, R, d0);
 }
 
-// int16 -> float via the 2^23 + 2^15 magic: bits (u ^ 0x4B008000) of the
-// zero-extended 16-bit value u are the float 2^23 + 2^15 + v.
 // int16 sample -> float: sign-extending shared load (LDS.S16) + I2FP.F32.S32
 // (the full-rate conversion; the compiler's own choice is LDS.U16 + the
 // quarter-rate I2F.S16).  `off` is a compile-time byte offset.
@@ -135,7 +126,6 @@ __device__ __forceinline__ float lds_s16f(uint32_t addr, int off) {
 }
 constexpr float kFloorMagic = 12582912.0f;  // 1.5 * 2^23
 constexpr int kFloorMagicBits = 0x4B400000;
-constexpr int kHalo = 64;                   // FIR halo (>= kMaxHalfTaps), each side
 
 __host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
 
@@ -143,72 +133,84 @@ __host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~si
 __host__ __device__ inline size_t stage_bytes(int FB, int rows) {
   return align128((size_t)FB * rows * kRowSamples * 2);
 }
-// FIR line buffer: ngroups x padded(S + 2 halo + 4) float4 (4 frames), with
-// a 16-byte pad after every 4 samples (conflict-free sliding LDS.128).
-__host__ __device__ inline int fir_pad(int kp) { return kp + (kp >> 2); }
-__host__ __device__ inline int fir_span(int S) { return fir_pad(S + 2 * kHalo + 4); }
-__host__ __device__ inline size_t fir_bytes(int FB, int S) {
-  return align128((size_t)((FB + 3) / 4) * fir_span(S) * 16);
-}
-
-// Stages in the trace ring: as many as fit a ~100 KB budget (2 CTAs/SM), 3..8.
-__host__ __device__ inline int das_stages(int FB, int S) {
-  const int n = (int)((100 * 1024) / stage_bytes(FB, das_rows(S)));
-  return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : n);
-}
+// FIR line buffer of one pass: RF at k in [k0 - 2P, k0 + PL + P + 4) for
+// ngroups = ceil(FB/4) frame groups, float4 = 4 frames, with a 16-byte pad
+// after every 4 samples (conflict-free sliding LDS.128).
+__host__ __device__ inline int fir_pad(int b) { return b + (b >> 2); }
+__host__ __device__ inline int fir_span(int PL, int P) { return fir_pad(PL + 3 * P + 4); }
+__host__ __device__ inline int fir_groups(int FB) { return (FB + 3) / 4; }
 
 struct SmemLayout {
   int16_t* stage;   // [NS][stage_bytes]
+  float4* line;     // FIR line buffer, aliases the stage ring between passes
   float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
   int2* wse;        // [nent] {window start ws, channel}
-  uint64_t* full;   // [NS]
-  unsigned* rel;    // [NS] warps done with the slot (last one refills it)
-  unsigned* smax;   // [8]
-  float4* line;     // FIR buffer, aliases the stage ring after the DAS loop
+  float4* carry;    // [ngroups][2P] RF tail of the previous pass
+  uint64_t* full;   // [kMaxStages]
+  unsigned* rel;    // [kMaxStages] warps done with the slot (last one refills it)
+  unsigned* smax;   // [16] per-frame envelope max (float bits)
 };
 
-__host__ __device__ inline size_t layout_bytes(int FB, int S, int nent_max, size_t* off) {
-  const int rows = das_rows(S);
-  const size_t ring = (size_t)das_stages(FB, S) * stage_bytes(FB, rows);
-  const size_t fb = fir_bytes(FB, S);
+// Bytes of everything except the ring; ring stages fill the rest of the
+// per-CTA budget (2 CTAs per SM), between 3 and kMaxStages.
+__host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P) {
+  return align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
+         align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1)) + align128(sizeof(uint64_t) * kMaxStages) +
+         align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16);
+}
+constexpr size_t kSmemBudget = 113 * 1024;
+
+__host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P) {
+  const size_t fixed = fixed_bytes(FB, nent_max, P);
+  const size_t sb = stage_bytes(FB, das_rows_nt(NT));
+  const long n = fixed >= kSmemBudget ? 0 : (long)((kSmemBudget - fixed) / sb);
+  return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : (int)n);
+}
+
+__host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int P, size_t* off) {
+  const size_t ring = (size_t)das_stages(FB, NT, nent_max, P) * stage_bytes(FB, das_rows_nt(NT));
+  const size_t fb = align128((size_t)fir_groups(FB) * fir_span(NT * kTileK, P) * 16);
   size_t o = 0;
   off[0] = o; o = align128(o + (ring > fb ? ring : fb));
   off[1] = o; o = align128(o + sizeof(float4) * nent_max);
   off[2] = o; o = align128(o + sizeof(int2) * nent_max);
-  off[3] = o; o = align128(o + sizeof(uint64_t) * kMaxStages);
-  off[4] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
-  off[5] = o; o = align128(o + sizeof(unsigned) * 8);
+  off[3] = o; o = align128(o + sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
+  off[4] = o; o = align128(o + sizeof(uint64_t) * kMaxStages);
+  off[5] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
+  off[6] = o; o = align128(o + sizeof(unsigned) * 16);
   return o;
 }
 
-__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int S, int nent_max) {
-  size_t off[6];
-  layout_bytes(FB, S, nent_max, off);
+__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT, int nent_max, int P) {
+  size_t off[7];
+  layout_bytes(FB, NT, nent_max, P, off);
   SmemLayout L;
   L.stage = (int16_t*)(base + off[0]);
   L.line = (float4*)(base + off[0]);
   L.rec = (float4*)(base + off[1]);
   L.wse = (int2*)(base + off[2]);
-  L.full = (uint64_t*)(base + off[3]);
-  L.rel = (unsigned*)(base + off[4]);
-  L.smax = (unsigned*)(base + off[5]);
+  L.carry = (float4*)(base + off[3]);
+  L.full = (uint64_t*)(base + off[4]);
+  L.rel = (unsigned*)(base + off[5]);
+  L.smax = (unsigned*)(base + off[6]);
   return L;
 }
 
 // ---------------------------------------------------------------------------
-// Epilogue: envelope of 4 consecutive outputs k0..k0+3 for the 4 frames of
-// one frame group (sliding window over the padded line buffer; x(k) = 0
-// outside [0, S)), then log compression or env + running max.
+// Epilogue: envelope of 4 consecutive outputs o0..o0+3 (< o_end) for the 4
+// frames of one frame group, sliding over the pass's line buffer (buffer
+// position b = k - kbase; RF outside [0, S) is zero in the buffer), then log
+// compression or env + running max.
 // b[k] = c0 x[k] + sum_{j>=1} c_j (x[k-j] + x[k+j]) + i s_j (x[k-j] - x[k+j])
 // (reading #18: g_j = h_j e^{+i w j}, h symmetric), env = 2 |b|.
 template <int FB>
-__device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int k0, int line, int fg0,
-                                          float* bmax) {
+__device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int kbase, int o0, int o_end,
+                                          int line, int fg0, float* bmax) {
   const int P = (a.fir_taps - 1) / 2;
-  auto X = [&](int k) { return lineg[fir_pad(k + kHalo)]; };
+  auto X = [&](int k) { return lineg[fir_pad(k - kbase)]; };
   float4 Lw[4], Rw[4];
 #pragma unroll
-  for (int o = 0; o < 4; o++) Lw[o] = Rw[o] = X(k0 + o);
+  for (int o = 0; o < 4; o++) Lw[o] = Rw[o] = X(o0 + o);
   float2 re[4][2], im[4][2];
   const float c0 = a.fir_c[0];
 #pragma unroll
@@ -220,9 +222,9 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
 #pragma unroll
   for (int j = 1; j <= kMaxHalfTaps; j++) {
     if (j > P) break;
-    // shift: Lw[o] = x[k0 + o - j], Rw[o] = x[k0 + o + j]
-    Lw[3] = Lw[2]; Lw[2] = Lw[1]; Lw[1] = Lw[0]; Lw[0] = X(k0 - j);
-    Rw[0] = Rw[1]; Rw[1] = Rw[2]; Rw[2] = Rw[3]; Rw[3] = X(k0 + 3 + j);
+    // shift: Lw[o] = x[o0 + o - j], Rw[o] = x[o0 + o + j]
+    Lw[3] = Lw[2]; Lw[2] = Lw[1]; Lw[1] = Lw[0]; Lw[0] = X(o0 - j);
+    Rw[0] = Rw[1]; Rw[1] = Rw[2]; Rw[2] = Rw[3]; Rw[3] = X(o0 + 3 + j);
     const float2 cj = make_float2(a.fir_c[j], a.fir_c[j]), sj = make_float2(a.fir_s[j], a.fir_s[j]);
 #pragma unroll
     for (int o = 0; o < 4; o++) {
@@ -236,8 +238,8 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
   }
 #pragma unroll
   for (int o = 0; o < 4; o++) {
-    const int k = k0 + o;
-    if (k >= a.S) break;
+    const int k = o0 + o;
+    if (k >= o_end) break;
     const float2 e0 = __ffma2_rn(re[o][0], re[o][0], __fmul2_rn(im[o][0], im[o][0]));
     const float2 e1 = __ffma2_rn(re[o][1], re[o][1], __fmul2_rn(im[o][1], im[o][1]));
     const float env[4] = {2.f * sqrtf(e0.x), 2.f * sqrtf(e0.y), 2.f * sqrtf(e1.x), 2.f * sqrtf(e1.y)};
@@ -282,27 +284,28 @@ struct Acc {
 // Specialisation granularity of the first active tile (code size).
 __host__ __device__ constexpr int tile_gran(int NT) { return NT <= 8 ? 1 : 2; }
 
-// One aperture entry, output tiles M0 .. NT-1 (straight-line).
+// One aperture entry, output tiles M0 .. NT-1 of the pass (straight-line).
+// kt0f = (float)(k0 + kt): the thread's first output sample in the pass.
 template <int FB, int NT, int M0, bool T0>
 __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, int kenter, int wsm,
-                                            const unsigned short* st, int kt, float ktf, int S,
+                                            const unsigned short* st, int kt, int k0, float kt0f,
                                             Acc<FB, NT>& acc) {
   constexpr int FR = (NT * 8 + 2) * kRowSamples;
 #pragma unroll
   for (int m = M0; m < NT; m++) {
-    const int k = m * kTileK + kt;
-    // k_enter < (M0 + gran) * 256, so only the first gran tiles can hold
-    // non-members.  Outputs k >= S (when S < 256 NT) are computed but never
-    // stored, and their taps stay inside the staged window.
+    const int k = k0 + m * kTileK + kt;
+    // the warp's first member tile is >= M0 and k_enter < k0 + (M0 + gran) * 256,
+    // so only the first gran tiles can hold non-members.  Outputs k >= S
+    // are computed but never stored; their taps stay inside the window.
     const bool first = m < M0 + tile_gran(NT);
     const bool mem = !first || k >= kenter;
-    const float kf = ktf + (float)(m * kTileK);
+    const float kf = kt0f + (float)(m * kTileK);
     const float h = 0.5f * kf;
-    const float h2 = (m == 0 && kt == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
+    const float h2 = (m == 0 && k == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
     float delta = split_delay(r.x, r.y, h, h2);
     if (T0) delta += a.t0fs;
     const float tf = __fadd_rd(delta, kFloorMagic);
-    int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - kt)
+    int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - k0 - kt)
     const float fr = delta - (tf - kFloorMagic);
     idx = mem ? idx : 0;
     // opaque copy: keeps one materialised index so the 2 FB loads below use
@@ -331,12 +334,12 @@ __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, i
 
 template <int FB, int NT, bool T0, int G = 0>
 __device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const float4& r, int kenter, int wsm,
-                                               const unsigned short* st, int kt, float ktf, int S,
+                                               const unsigned short* st, int kt, int k0, float kt0f,
                                                Acc<FB, NT>& acc) {
   constexpr int M0 = G * tile_gran(NT);
   if constexpr (M0 < NT) {
-    if (g == G) entry_tiles<FB, NT, M0, T0>(a, r, kenter, wsm, st, kt, ktf, S, acc);
-    else dispatch_tiles<FB, NT, T0, G + 1>(g, a, r, kenter, wsm, st, kt, ktf, S, acc);
+    if (g == G) entry_tiles<FB, NT, M0, T0>(a, r, kenter, wsm, st, kt, k0, kt0f, acc);
+    else dispatch_tiles<FB, NT, T0, G + 1>(g, a, r, kenter, wsm, st, kt, k0, kt0f, acc);
   }
 }
 
@@ -344,19 +347,26 @@ template <int FB, int NT, bool T0>
 __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const DasArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int S = a.S;
+  constexpr int PL = NT * kTileK;                 // samples per pass
   constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
+  const int S = a.S;
+  const int P = (a.fir_taps - 1) / 2;
   const size_t SB = stage_bytes(FB, NT * 8 + 2);
-  SmemLayout sm = carve(smem_raw, FB, S, a.entries_per_group);
+  SmemLayout sm = carve(smem_raw, FB, NT, a.entries_per_group, P);
   const int line = a.line0 + blockIdx.x;
-  const int f0 = blockIdx.y * FB;
+  const int fm = blockIdx.y * FB;   // first frame of the CTA in the tensor map
+  const int f0 = a.fbase + fm;      // ... and in the call
+  if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int g = a.line_group[line];
   const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
   const int nent = a.nentries[g];
   const int lane = threadIdx.x & 31;
   const int ev = a.line_event[line];
+  const float4 dir = a.line_dir[line];
+  const int NS = das_stages(FB, NT, a.entries_per_group, P);
+  const int ng = fir_groups(FB);
+  const int span = fir_span(PL, P);
 
-  const int NS = das_stages(FB, S);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; i++) {
       mbar_init(&sm.full[i], 1);
@@ -365,57 +375,78 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
-  if (threadIdx.x < 8) sm.smax[threadIdx.x] = 0u;
-  // Entry records for this line, computed once in parallel:
-  // window [ws, ws + rows*32), rows = 8 NT + 2 >= S/32 + 2,
-  // ws <= floor(tau(k_enter)) - 2 and 32-aligned: d tau/dk in [0, 1] gives
-  // i0(k) + 1 <= ws + S + 34 for every member k < S, inside the window;
-  // reads past the record (>= S) or before it (< 0) come back as TMA zeros.
-  {
-    const float4 dir = a.line_dir[line];
-    for (int i = threadIdx.x; i < nent; i += blockDim.x) {
-      const DasEntry e = ents[i];
+  if (threadIdx.x < 16) sm.smax[threadIdx.x] = 0u;
+
+  const int kt = threadIdx.x;
+  const int kwarp_last = (kt | 31);
+  float bmax[4] = {0.f, 0.f, 0.f, 0.f};
+  int curg = -1;
+  int buf = 0;           // ring slot of the next entry (continues across passes)
+  unsigned phase = 0;    // its mbarrier parity
+  auto flush_max = [&]() {
+    if (curg >= 0 && !a.ref_fixed)
+      for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
+  };
+
+  for (int k0 = 0; k0 < S; k0 += PL) {
+    const int kend = min(S, k0 + PL);
+    // entries with a member sample in the pass: the k_enter-sorted prefix
+    // with k_enter < kend
+    int np = 0;
+    for (int i0 = 0; i0 < nent; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      np += __syncthreads_count(i < nent && ents[i].kenter < kend);
+    }
+    // Entry records of the pass, in device order: alternate the long-trace
+    // (early k_enter) and short-trace ends of the prefix so consecutive
+    // ring entries carry similar work.  Window [ws, ws + rows*32),
+    // rows = PL/32 + 2, ws <= floor(tau(kb)) - 2 and 32-aligned, kb =
+    // max(k_enter, k0): d tau/dk in [0, 1] keeps i0(k) + 1 inside the
+    // window for every member k of the pass; reads outside the record come
+    // back as TMA zeros.  (The sum order is fixed per configuration: results
+    // are deterministic and identical across frames and batch sizes.)
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+      const DasEntry e = ents[(i & 1) ? np - 1 - i / 2 : i / 2];
       const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
       const float Ah = 0.5f * e.A;
-      const int kb = e.kenter;
+      const int kb = max(e.kenter, k0);
       const float hb = 0.5f * (float)kb;
       const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
       const int ws = ((int)floorf(tb) - 2) & ~(kRowSamples - 1);
-      sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(kb));
+      sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(e.kenter));
       sm.wse[i] = make_int2(ws, e.elem);
     }
-  }
-  __syncthreads();
+    __syncthreads();  // records visible; the previous pass is done with the line buffer
 
-  // Producer step: TMA of entry jj's trace (all FB frames) into slot buf.
-  auto produce = [&](int jj, int buf) {
-    const int2 we = sm.wse[jj];
-    mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
-    tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, we.x / kRowSamples, we.y, ev, f0, &sm.full[buf]);
-  };
-  if (threadIdx.x == 0 && a.debug_skip != 2)
-    for (int jj = 0; jj < NS && jj < nent; jj++) produce(jj, jj);
+    // TMA of entry jj's window (all FB frames) into ring slot `buf`.
+    auto produce = [&](int jj, int buf) {
+      const int2 we = sm.wse[jj];
+      mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
+      tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, we.x / kRowSamples, we.y, ev, fm, &sm.full[buf]);
+    };
+    if (threadIdx.x == 0 && a.debug_skip != 2) {
+      // the ring was last written through the generic proxy (line buffer)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int jj = 0, b = buf; jj < NS && jj < np; jj++, b = (b + 1 == NS ? 0 : b + 1)) produce(jj, b);
+    }
 
-  {
-    // ------------------------------ consumers -----------------------------
-    const int kt = threadIdx.x;
-    const float ktf = (float)kt;
     Acc<FB, NT> acc;
     acc.zero();
-    int buf = 0;
-    unsigned phase = 0;
-    for (int j = 0; j < nent; j++) {
+    const float kt0f = (float)(k0 + kt);
+    for (int j = 0; j < np; j++) {
       if (a.debug_skip != 2) mbar_wait(&sm.full[buf], phase);
       const float4 r = sm.rec[j];
       const int kenter = __float_as_int(r.w);
-      const int wsm = sm.wse[j].x + kFloorMagicBits - kt;
+      const int wsm = sm.wse[j].x + kFloorMagicBits - k0 - kt;
       const unsigned short* st = (const unsigned short*)((const unsigned char*)sm.stage + buf * SB);
-      // straight-line code for the tiles at or after the entry's first
-      // active tile (no per-tile branches: the chains of consecutive tiles
-      // interleave)
-      if (a.debug_skip != 1)
-        dispatch_tiles<FB, NT, T0>(min(kenter / kTileK, NT - 1) / tile_gran(NT), a, r, kenter, wsm, st, kt, ktf, S,
-                                   acc);
+      // first tile of the pass in which this WARP has a member sample
+      // (warp-uniform): straight-line code from there (the chains of
+      // consecutive tiles interleave); tiles where all 32 of the warp's k
+      // are < k_enter are skipped.
+      int m0 = kenter - k0 - kwarp_last;
+      m0 = m0 <= 0 ? 0 : (m0 + kTileK - 1) / kTileK;
+      if (a.debug_skip != 1 && m0 < NT)
+        dispatch_tiles<FB, NT, T0>(m0 / tile_gran(NT), a, r, kenter, wsm, st, kt, k0, kt0f, acc);
       // release the slot; the last warp to release it refills it (no warp
       // ever waits for another to issue a copy)
       __syncwarp();
@@ -423,7 +454,7 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
         const unsigned prev = atom_add_acqrel(&sm.rel[buf], 1u);
         if (prev == (blockDim.x / 32) - 1) {
           sm.rel[buf] = 0u;
-          if (j + NS < nent && a.debug_skip != 2) {
+          if (j + NS < np && a.debug_skip != 2) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             produce(j + NS, buf);
           }
@@ -434,34 +465,38 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
         phase ^= 1u;
       }
     }
+    __syncthreads();  // every warp is done with the ring: it becomes the line buffer
+
     // ---- RF = sum / N (reading #7; 0 when N = 0) ----
     const uint16_t* ncount = a.ncount + (size_t)g * S;
-    __syncthreads();  // every warp is done with the trace ring (aliased below)
-    const int span = fir_span(S);
+    const int kbase = k0 - 2 * P;  // line buffer position b = k - kbase
 #pragma unroll
     for (int m = 0; m < NT; m++) {
-      if (m * kTileK >= S) break;
-      const int k = m * kTileK + kt;
-      if (k >= S) break;
-      const int n = (int)ncount[k];
-      const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
+      const int k = k0 + m * kTileK + kt;
       float v[FB];
-      if constexpr (FB == 1) {
-        v[0] = acc.s[m] * inv;
+      if (k < S) {
+        const int n = (int)ncount[k];
+        const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
+        if constexpr (FB == 1) {
+          v[0] = acc.s[m] * inv;
+        } else {
+#pragma unroll
+          for (int q = 0; q < FB / 2; q++) {
+            v[2 * q] = acc.p[m][q].x * inv;
+            v[2 * q + 1] = acc.p[m][q].y * inv;
+          }
+        }
+        if (a.rf) {
+#pragma unroll
+          for (int b = 0; b < FB; b++)
+            if (f0 + b < a.F) a.rf[((size_t)(f0 + b) * a.L + line) * S + k] = v[b];
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < FB / 2; q++) {
-          v[2 * q] = acc.p[m][q].x * inv;
-          v[2 * q + 1] = acc.p[m][q].y * inv;
-        }
-      }
-      if (a.rf) {
-#pragma unroll
-        for (int b = 0; b < FB; b++)
-          if (f0 + b < a.F) a.rf[((size_t)(f0 + b) * a.L + line) * S + k] = v[b];
+        for (int b = 0; b < FB; b++) v[b] = 0.f;  // zero padding past the record
       }
       if (a.do_epilogue) {
-        const int pk = fir_pad(k + kHalo);
+        const int pk = fir_pad(k - kbase);
 #pragma unroll
         for (int q4 = 0; q4 < (FB + 3) / 4; q4++) {
           float4 x;
@@ -473,68 +508,101 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
         }
       }
     }
-  }
-  if (!a.do_epilogue) return;
-  const int ng = (FB + 3) / 4, span = fir_span(S);
-  // zero halos: padded positions of k' in [0, kHalo) and [kHalo + S, S + 2 kHalo + 4)
-  for (int i = threadIdx.x; i < ng * (2 * kHalo + 4); i += blockDim.x) {
-    const int q4 = i / (2 * kHalo + 4), r = i - q4 * (2 * kHalo + 4);
-    const int kp = r < kHalo ? r : S + r;
-    sm.line[(size_t)q4 * span + fir_pad(kp)] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncthreads();
-  // ---- epilogue: work items = (frame group, 4 consecutive outputs) ----
-  const int nblk = (S + 3) / 4;
-  float bmax[4] = {0.f, 0.f, 0.f, 0.f};
-  int curg = -1;
-  for (int it = threadIdx.x; it < ng * nblk; it += blockDim.x) {
-    const int q4 = it / nblk, blk = it - q4 * nblk;
-    if (q4 != curg) {
-      if (curg >= 0 && !a.ref_fixed)
-        for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
-      curg = q4;
-      bmax[0] = bmax[1] = bmax[2] = bmax[3] = 0.f;
+    if (!a.do_epilogue) continue;
+    // carried RF tail (or zeros before k = 0) and zeros after the pass
+    const int tail = P + 4;
+    for (int i = threadIdx.x; i < ng * (2 * P + tail); i += blockDim.x) {
+      const int q4 = i / (2 * P + tail), r = i - q4 * (2 * P + tail);
+      if (r < 2 * P)
+        sm.line[(size_t)q4 * span + fir_pad(r)] =
+            k0 == 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : sm.carry[q4 * 2 * P + r];
+      else
+        sm.line[(size_t)q4 * span + fir_pad(PL + r)] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    fir_block<FB>(a, sm.line + (size_t)q4 * span, 4 * blk, line, f0 + 4 * q4, bmax);
+    __syncthreads();
+    // ---- epilogue: outputs whose taps are complete in this pass ----
+    const int o_begin = k0 == 0 ? 0 : k0 - P;
+    const int o_end = kend == S ? S : k0 + PL - P;
+    const int nblk = (o_end - o_begin + 3) / 4;
+    for (int it = threadIdx.x; it < ng * nblk; it += blockDim.x) {
+      const int q4 = it / nblk, blk = it - q4 * nblk;
+      if (q4 != curg) {
+        flush_max();
+        curg = q4;
+        bmax[0] = bmax[1] = bmax[2] = bmax[3] = 0.f;
+      }
+      fir_block<FB>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, line, f0 + 4 * q4, bmax);
+    }
+    // RF tail k in [k0 + PL - 2P, k0 + PL) for the next pass's first outputs
+    if (kend < S)
+      for (int i = threadIdx.x; i < ng * 2 * P; i += blockDim.x) {
+        const int q4 = i / (2 * P), r = i - q4 * 2 * P;
+        sm.carry[i] = sm.line[(size_t)q4 * span + fir_pad(PL + r)];
+      }
+    // (the __syncthreads at the top of the next pass orders these reads
+    // before the ring is refilled)
   }
-  if (!a.ref_fixed) {
-    if (curg >= 0)
-      for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
+  if (a.do_epilogue && !a.ref_fixed) {
+    flush_max();
     __syncthreads();
     if (threadIdx.x < FB && f0 + (int)threadIdx.x < a.F)
       atomicMax(&a.frame_max[f0 + threadIdx.x], sm.smax[threadIdx.x]);
   }
+  // secondary launch of a split call: complete only after the primary grid
+  // (so work queued behind this kernel also sees the primary's results)
+  if (a.pdl_wait_end) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-size_t das_smem_bytes(int FB, int S, int nent_max) {
-  size_t off[6];
-  return layout_bytes(FB, S, nent_max, off);
+size_t das_smem_bytes(int FB, int NT, int nent_max, int fir_taps) {
+  size_t off[7];
+  return layout_bytes(FB, NT, nent_max, (fir_taps - 1) / 2, off);
 }
 
-// Frames per CTA: registers hold NT x FB accumulators (<= 64), the smem
-// footprint must allow 2 CTAs per SM, and never more frames than the call.
-int das_frames_per_cta(int fb_max, int S, int F, int nent_max) {
-  const int nt = das_nt(S);
-  int fb = fb_max;
-  while (fb > 1 && (fb > F || fb * nt > 64 || das_smem_bytes(fb, S, nent_max) > 113 * 1024)) fb >>= 1;
-  return fb;
+// (frames per CTA, tiles per pass): the first feasible candidate -- FB x NT
+// accumulators <= 64 per thread, passes no longer than the record, the
+// shared-memory footprint allows 2 CTAs per SM with >= 3 ring stages, and
+// never more frames than the call (or fb_max).
+DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps) {
+  static const int cand[][2] = {{16, 4}, {8, 8}, {8, 4}, {4, 16}, {4, 8}, {4, 4}, {2, 16},
+                                {2, 8},  {2, 4}, {1, 16}, {1, 8}, {1, 4}};
+  const int ntmax = das_nt(S);
+  const int P = (fir_taps - 1) / 2;
+  for (auto& c : cand) {
+    const int fb = c[0], nt = c[1];
+    if (fb > fb_max || (fb > F && fb > 1) || nt > ntmax) continue;
+    const size_t fixed = fixed_bytes(fb, nent_max, P);
+    const size_t ring = 3 * stage_bytes(fb, das_rows_nt(nt));
+    const size_t fir = align128((size_t)fir_groups(fb) * fir_span(nt * kTileK, P) * 16);
+    if (fixed + (ring > fir ? ring : fir) > kSmemBudget) continue;
+    return DasShape{fb, nt};
+  }
+  return DasShape{1, 4};
 }
 
 template <int FB, int NT, bool T0>
 static cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
-  const size_t smem = das_smem_bytes(FB, a.S, a.entries_per_group);
+  const size_t smem = das_smem_bytes(FB, NT, a.entries_per_group, a.fir_taps);
   auto kern = das_fused_kernel<FB, NT, T0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(a.nlines, (a.F + FB - 1) / FB);
-  kern<<<grid, 256, smem, st>>>(tm, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.nlines, (a.Fmap + FB - 1) / FB);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl_wait_end ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, tm, a);
 }
 
 template <bool T0>
-static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, int fb, cudaStream_t st) {
-  const int nt = das_nt(a.S);
-  switch (fb) {
+static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, DasShape sh, cudaStream_t st) {
+  const int nt = sh.nt;
+  switch (sh.fb) {
+    case 16: return launch_k<16, 4, T0>(tm, a, st);
     case 8: return nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st);
     case 4:
       return nt == 4 ? launch_k<4, 4, T0>(tm, a, st)
@@ -548,8 +616,8 @@ static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, int fb, cu
   }
 }
 
-cudaError_t launch_das(const CUtensorMap& tm, const DasArgs& a, int fb, cudaStream_t st) {
-  return a.t0fs != 0.f ? launch_t0<true>(tm, a, fb, st) : launch_t0<false>(tm, a, fb, st);
+cudaError_t launch_das(const CUtensorMap& tm, const DasArgs& a, DasShape sh, cudaStream_t st) {
+  return a.t0fs != 0.f ? launch_t0<true>(tm, a, sh, st) : launch_t0<false>(tm, a, sh, st);
 }
 
 }  // namespace supra

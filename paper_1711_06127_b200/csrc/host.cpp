@@ -283,15 +283,12 @@ supra_status build_das_tables(supra_bf* h) {
   std::vector<int32_t> nentries(G);
   std::vector<uint16_t> ncount((size_t)G * S);
   for (int g = 0; g < G; g++) {
-    // Device order: alternate the long-trace (early k_enter) and short-trace
-    // (late k_enter) ends of the sorted list, so consecutive entries in the
-    // TMA ring carry similar work and the prefetch depth in time stays even.
-    // (Sum order is fixed per configuration: results stay deterministic and
-    // identical across frames and batch sizes.)
+    // ascending k_enter; the kernel takes the prefix of entries that are
+    // members within a depth pass and interleaves its two ends itself
     const int n = (int)groups[g].size();
     for (int j = 0; j < per; j++) {
       DasEntry d{};
-      if (j < n) d = groups[g][(j & 1) ? n - 1 - j / 2 : j / 2];
+      if (j < n) d = groups[g][j];
       else { d.kenter = 0x7fffffff; }
       flat[(size_t)g * per + j] = d;
     }
@@ -539,16 +536,16 @@ EncodeTiledFn encode_fn() {
 }
 
 // raw [F][E][C][S] int16 viewed as u32 sample pairs in rows of 16 pairs:
-// dims {16, S/32, C, E, F}; box {16, das_rows(S), 1, 1, fb} -- one TMA per
-// (aperture entry, frame group) fetches a whole trace; out-of-bounds rows
-// (before 0 or past S) and frames (>= F) read as zero.
-bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, int fb) {
+// dims {16, S/32, C, E, F}; box {16, rows, 1, 1, fb} -- one TMA per
+// (aperture entry, depth pass, frame group) fetches the pass's trace window;
+// out-of-bounds rows (before 0 or past S) and frames (>= F) read as zero.
+bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, int rows, int fb) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[5] = {16, (cuuint64_t)S / kRowSamples, (cuuint64_t)C, (cuuint64_t)E, (cuuint64_t)F};
   cuuint64_t strides[4] = {(cuuint64_t)kRowSamples * 2, (cuuint64_t)S * 2, (cuuint64_t)C * S * 2,
                            (cuuint64_t)E * C * S * 2};
-  cuuint32_t box[5] = {16, (cuuint32_t)das_rows(S), 1, 1, (cuuint32_t)fb};
+  cuuint32_t box[5] = {16, (cuuint32_t)rows, 1, 1, (cuuint32_t)fb};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<void*>(raw), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -618,12 +615,12 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   }
   // DAS launch shape
   const int maxF = cfg->max_frames_per_call;
-  h->frames_per_cta = das_frames_per_cta(8, h->S, maxF, h->entries_per_group);
+  h->frames_per_cta = 16;  // upper bound; das_shape() picks per call
   if (const char* ev = std::getenv("SUPRA_BF_FRAMES_PER_CTA")) {
     int v = std::atoi(ev);
-    if (v == 1 || v == 2 || v == 4 || v == 8) h->frames_per_cta = das_frames_per_cta(v, h->S, maxF, h->entries_per_group);
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) h->frames_per_cta = v;
   }
-  h->das_smem = das_smem_bytes(h->frames_per_cta, h->S, h->entries_per_group);
+  const DasShape sh = das_shape(h->frames_per_cta, h->S, maxF, h->entries_per_group, cfg->fir_taps);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
   if (e == cudaSuccess && cfg->reference_mode == SUPRA_REF_FRAME_MAX && cfg->line_output_type == SUPRA_T_U8)
     e = cudaMalloc((void**)&h->d_env, sizeof(float) * (size_t)maxF * h->L * h->S);
@@ -632,9 +629,10 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
     delete h;
     return fail(SUPRA_E_RESOURCE, "scratch allocation: %s", cudaGetErrorString(e));
   }
-  h->info[0] = (cfg->reference_mode == SUPRA_REF_FRAME_MAX) ? 2 : 1;
-  h->info[1] = h->frames_per_cta;
-  h->info[2] = kTileK;
+  // kernels per beamform call at max_frames_per_call: DAS (+ remainder DAS) (+ finalize)
+  h->info[0] = 1 + (maxF % sh.fb != 0) + (cfg->reference_mode == SUPRA_REF_FRAME_MAX);
+  h->info[1] = sh.fb;
+  h->info[2] = (int64_t)sh.nt * kTileK;
   *out = h;
   return SUPRA_OK;
 }
@@ -674,9 +672,7 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.C = h->C;
   a.S = h->S;
   a.L = h->L;
-  a.ntiles = h->ntiles;
   a.entries_per_group = h->entries_per_group;
-  a.rows = das_rows(h->S);
   a.line_group = h->d_line_group;
   a.entries = h->d_entries;
   a.nentries = h->d_nentries;
@@ -716,12 +712,33 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
-  const int fb = das_frames_per_cta(h->frames_per_cta, h->S, frames, h->entries_per_group);
-  CUtensorMap tm;
-  if (!make_raw_map(&tm, raw, frames, h->E, h->C, h->S, fb))
+  // Frames in groups of sh.fb per CTA; a remainder (frames % fb) runs as a
+  // second, programmatically-serialised launch with its own (smaller) shape
+  // that fills the SMs the first grid's tail leaves idle.
+  const DasShape sh = das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps);
+  const int Fmain = (frames / sh.fb) * sh.fb;
+  const int rem = frames - Fmain;
+  const DasShape sh2 = rem ? das_shape(h->frames_per_cta, h->S, rem, h->entries_per_group, c.fir_taps) : sh;
+  const size_t frame_bytes = (size_t)h->E * h->C * h->S * sizeof(int16_t);
+  CUtensorMap tm, tm2;
+  if (!make_raw_map(&tm, raw, Fmain, h->E, h->C, h->S, das_rows_nt(sh.nt), sh.fb) ||
+      (rem && !make_raw_map(&tm2, (const char*)raw + Fmain * frame_bytes, rem, h->E, h->C, h->S,
+                            das_rows_nt(sh2.nt), sh2.fb)))
     return fail(SUPRA_E_CUDA, "cuTensorMapEncodeTiled failed for the raw buffer");
+  a.fbase = 0;
+  a.Fmap = Fmain;
+  a.pdl_trigger = rem > 0;
+  a.pdl_wait_end = 0;
   if (h->ev_before) cudaEventRecord(h->ev_before, st);
-  supra_status s = check_launch(launch_das(tm, a, fb, st), "das kernel");
+  supra_status s = check_launch(launch_das(tm, a, sh, st), "das kernel");
+  if (s == SUPRA_OK && rem) {
+    DasArgs a2 = a;
+    a2.fbase = Fmain;
+    a2.Fmap = rem;
+    a2.pdl_trigger = 0;
+    a2.pdl_wait_end = 1;
+    s = check_launch(launch_das(tm2, a2, sh2, st), "das kernel (remainder frames)");
+  }
   if (h->ev_after) cudaEventRecord(h->ev_after, st);
   if (s != SUPRA_OK || !line_img || a.ref_fixed || env_ext) return s;
   FinalizeArgs fa{};

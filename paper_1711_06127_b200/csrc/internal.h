@@ -21,13 +21,18 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxHalfTaps = 64;
 // Largest record the DAS kernel holds per line (NT = 16 tiles).
 constexpr int kMaxSamples = 16 * kTileK;
-// Output tiles per thread (a template parameter of the DAS kernel) and the
+// Output tiles per thread and pass (a template parameter of the DAS kernel,
+// NT in {4, 8, 16}; a pass covers kTileK * NT samples of depth) and the
 // trace rows one TMA box fetches for that NT (the stage's frame stride).
-inline __host__ __device__ int das_nt(int S) {
+inline __host__ __device__ int das_nt(int S) {  // largest useful NT for S
   const int t = (S + kTileK - 1) / kTileK;
   return t <= 4 ? 4 : (t <= 8 ? 8 : 16);
 }
-inline __host__ __device__ int das_rows(int S) { return das_nt(S) * (kTileK / kRowSamples) + 2; }
+inline __host__ __device__ int das_rows_nt(int nt) { return nt * (kTileK / kRowSamples) + 2; }
+// DAS launch shape: frames per CTA (fb) x tiles per pass (nt), fb * nt <= 64.
+struct DasShape {
+  int fb, nt;
+};
 
 // One receive-aperture entry of a line group (lines sharing an origin),
 // sorted by k_enter.  Lengths in "sample units" (mm * fs / (1000 c)), in
@@ -44,12 +49,13 @@ struct __align__(16) DasEntry {
 struct DasArgs {
   const int16_t* raw;      // [F][E][C][S]
   int F, E, C, S, L;
-  int ntiles;              // ceil(S / kTileK)
   int entries_per_group;   // row stride of `entries`
-  int rows;                // trace rows per TMA box: S / kRowSamples + 2
   int line0, nlines;           // lines [line0, line0 + nlines) of every frame are beamformed
+  int fbase, Fmap;             // frames [fbase, fbase + Fmap) of the call, = frames [0, Fmap) of the tensor map
+  int pdl_trigger;             // primary of a split call: let the secondary start on free SMs
+  int pdl_wait_end;            // secondary: launched programmatically, retire after the primary
   const int32_t* line_group;   // [L]
-  const DasEntry* entries;     // [G][entries_per_group], sorted by kenter
+  const DasEntry* entries;     // [G][entries_per_group], sorted by kenter (ascending)
   const int32_t* nentries;     // [G]: entries with kenter < S
   const uint16_t* ncount;      // [G][S]: N(k) = #entries with kenter <= k
   const float4* line_dir;      // [L] (dx, dy, dz, 0)
@@ -163,10 +169,10 @@ __device__ __forceinline__ float lg2_approx(float x) {
 
 // Launchers (return cudaGetLastError()).
 // raw is addressed through a 5-D tensor map {16 sample pairs (u32), S/32
-// rows, C, E, F} with box {16, rows, 1, 1, fb}; fb = das_frames_per_cta().
-cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, int fb, cudaStream_t st);
-int das_frames_per_cta(int fb_max, int S, int F, int nent_max);
-size_t das_smem_bytes(int frames_per_cta, int S, int nent_max);
+// rows, C, E, F} with box {16, das_rows_nt(nt), 1, 1, fb} for sh = das_shape().
+cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, DasShape sh, cudaStream_t st);
+DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps);
+size_t das_smem_bytes(int fb, int nt, int nent_max, int fir_taps);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st);
