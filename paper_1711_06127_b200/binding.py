@@ -14,7 +14,9 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsupra_bf.so")
+# SUPRA_BF_LIB: dev-only override with another build of the same library
+# (A/B measurements of kernel variants); the default is the in-tree build.
+LIB_PATH = os.environ.get("SUPRA_BF_LIB") or os.path.join(HERE, "libsupra_bf.so")
 
 ABI_VERSION = 1
 OK, E_PARAM, E_STRUCT, E_RESOURCE, E_CUDA = 0, 2, 3, 4, 5

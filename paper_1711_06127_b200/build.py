@@ -31,8 +31,16 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, variant: str = "",
+          defines=()) -> str:
+    """Build the library; ``variant``/``defines`` build an A/B variant into
+    _variants/<variant>/libsupra_bf.so (dev aid, selected with SUPRA_BF_LIB)."""
+    global BUILD, OUT
+    if variant:
+        BUILD = os.path.join(ROOT, "_variants", variant, "_build")
+        OUT = os.path.join(ROOT, "_variants", variant, "libsupra_bf.so")
     os.makedirs(BUILD, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     hdr_deps = [os.path.join(CSRC, h) for h in HDRS] + [os.path.join(ROOT, "include", "supra_bf.h")]
     objs = []
@@ -41,7 +49,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         obj = os.path.join(BUILD, f + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdr_deps):
-            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-O3", "-lineinfo", "-std=c++17",
+            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, *dflags, "-O3", "-lineinfo", "-std=c++17",
                    "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", *inc, "-c", src, "-o", obj]
             if ptxas_v:
                 cmd.insert(1, "-Xptxas=-v")
@@ -51,7 +59,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         obj = os.path.join(BUILD, f + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdr_deps):
-            _run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+            _run(["g++", *dflags, "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
                   "-Wall", "-I", os.path.join(CUDA, "include"), *inc, "-c", src, "-o", obj], verbose)
     if force or _stale(OUT, objs):
         _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-o", OUT, *objs,
@@ -60,5 +68,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv, variant=var, defines=defs)
     print(OUT)

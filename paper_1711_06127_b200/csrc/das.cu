@@ -29,6 +29,9 @@
 // frame-max reference (finalised by finalize_kernel).
 #include "internal.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace supra {
 
 namespace {
@@ -100,6 +103,15 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
   return r;
 }
 
+__device__ __forceinline__ float2 add_rm2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rm.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
 // delta = |q + h d| - h (samples), cancellation-free (reading #30).  With
 // hn = (|q|^2 + 2h d.q)/2:  r2 = h^2 + 2 hn,  y ~ 1/sqrt(r2) (MUFU.RSQ),
 // d0 = r2 y - h, and one Newton step on delta(delta + 2h) = 2 hn:
@@ -112,6 +124,20 @@ __device__ __forceinline__ float split_delay(float Ah, float B, float h, float h
   const float s = fmaf(d0, -0.5f, -h);
   const float R = fmaf(d0, s, hn);
   return fmaf(y, R, d0);
+}
+
+// The same for two output samples at once (packed f32x2: FFMA2 per step,
+// two MUFU.RSQ); per lane the operations and their order are those of
+// split_delay, so the results are identical.
+__device__ __forceinline__ float2 split_delay2(float Ah, float B, float2 h, float2 h2) {
+  const float2 hn = __ffma2_rn(h, make_float2(B, B), make_float2(Ah, Ah));
+  const float2 r2 = __ffma2_rn(hn, make_float2(2.0f, 2.0f), h2);
+  const float2 y = make_float2(rsqrt_ftz(r2.x), rsqrt_ftz(r2.y));
+  const float2 nh = make_float2(-h.x, -h.y);
+  const float2 d0 = __ffma2_rn(r2, y, nh);
+  const float2 s = __ffma2_rn(d0, make_float2(-0.5f, -0.5f), nh);
+  const float2 R = __ffma2_rn(d0, s, hn);
+  return __ffma2_rn(y, R, d0);
 }
 
 // int16 sample -> float: sign-extending shared load (LDS.S16) + I2FP.F32.S32
@@ -158,12 +184,16 @@ __host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P) {
          align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1)) + align128(sizeof(uint64_t) * kMaxStages) +
          align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16);
 }
-constexpr size_t kSmemBudget = 113 * 1024;
+// CTAs per SM: 3 for short passes (NT = 2: 32 accumulators, <= 85
+// registers), else 2; the per-CTA shared-memory budget follows.
+__host__ __device__ constexpr int das_ctas_per_sm(int NT) { return NT == 2 ? 3 : 2; }
+__host__ __device__ constexpr size_t das_smem_budget(int NT) { return NT == 2 ? 75 * 1024 : 113 * 1024; }
 
 __host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P) {
   const size_t fixed = fixed_bytes(FB, nent_max, P);
   const size_t sb = stage_bytes(FB, das_rows_nt(NT));
-  const long n = fixed >= kSmemBudget ? 0 : (long)((kSmemBudget - fixed) / sb);
+  const size_t budget = das_smem_budget(NT);
+  const long n = fixed >= budget ? 0 : (long)((budget - fixed) / sb);
   return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : (int)n);
 }
 
@@ -264,70 +294,145 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
 }  // namespace
 
 // Accumulators of one thread: NT output samples x FB frames.
+// FB = 1: tiles (2i, 2i+1) packed in s2[i]; FB >= 2: frame pairs in p[m][q].
 template <int FB, int NT>
 struct Acc {
-  float s[FB == 1 ? NT : 1];
+  float2 s2[FB == 1 ? NT / 2 : 1];
   float2 p[FB >= 2 ? NT : 1][FB >= 2 ? FB / 2 : 1];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       if constexpr (FB == 1) {
-        s[m] = 0.f;
+        if (m % 2 == 0) s2[m / 2] = make_float2(0.f, 0.f);
       } else {
 #pragma unroll
         for (int q = 0; q < FB / 2; q++) p[m][q] = make_float2(0.f, 0.f);
       }
     }
   }
+  __device__ __forceinline__ float s(int m) const { return (m & 1) ? s2[m / 2].y : s2[m / 2].x; }
+};
+
+// Per-tile tap geometry: index of x[i0] in the staged window and the two
+// interpolation weights.
+struct TapGeo {
+  int idx;
+  float w0, w1;
 };
 
 // Specialisation granularity of the first active tile (code size).
 __host__ __device__ constexpr int tile_gran(int NT) { return NT <= 8 ? 1 : 2; }
 
-// One aperture entry, output tiles M0 .. NT-1 of the pass (straight-line).
+// Accumulate one tile's tap for all FB frames (per frame pair: 4 sign-
+// extending LDS.S16 + I2FP, 2 FFMA2; frames at immediate offsets).
+template <int FB, int NT>
+__device__ __forceinline__ void tile_accumulate(const TapGeo& g, const unsigned short* st, float2* accp) {
+  constexpr int FR = (NT * 8 + 2) * kRowSamples;
+  int idx = g.idx;
+  // opaque copy: keeps one materialised index so the FB loads below use
+  // immediate offsets instead of one address add each
+  asm("mov.b32 %0, %0;" : "+r"(idx));
+  const uint32_t pa = smem_u32(st) + 2u * (uint32_t)idx;
+#pragma unroll
+  for (int q = 0; q < FB / 2; q++) {
+#if defined(SUPRA_EXP_NO_X1)  // measurement only: wrong numerics
+    const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
+    const float2 x1 = make_float2(x0.y, x0.x);
+#else
+    const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
+    const float2 x1 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR + 2), lds_s16f(pa, 2 * (2 * q + 1) * FR + 2));
+#endif
+    accp[q] = __ffma2_rn(make_float2(g.w0, g.w0), x0, accp[q]);
+    accp[q] = __ffma2_rn(make_float2(g.w1, g.w1), x1, accp[q]);
+  }
+}
+
+// Geometry of tile m alone (scalar).  The warp's first member tile is >= M0
+// and k_enter < k0 + (M0 + gran) * 256, so only the first gran tiles can
+// hold non-members (their weight and index are zeroed).  Outputs k >= S are
+// computed but never stored; their taps stay inside the window.
+template <int NT, int M0, bool T0>
+__device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4& r, int kenter, int wsm,
+                                           int kt, int k0, float kt0f) {
+  const int k = k0 + m * kTileK + kt;
+  const bool mem = !(m < M0 + tile_gran(NT)) || k >= kenter;
+  const float kf = kt0f + (float)(m * kTileK);
+  const float h = 0.5f * kf;
+  const float h2 = (m == 0 && k == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
+  float delta = split_delay(r.x, r.y, h, h2);
+  if (T0) delta += a.t0fs;
+  const float tf = __fadd_rd(delta, kFloorMagic);
+  const int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - k0 - kt)
+  const float fr = delta - (tf - kFloorMagic);
+  float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
+  w = mem ? w : 0.f;
+  // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
+  const float w1 = w * fr;
+  return TapGeo{mem ? idx : 0, w - w1, w1};
+}
+
+// Geometry of tiles m, m+1 together in packed f32x2 (FFMA2 / FADD2.RM /
+// FMUL2: about 40 % fewer issued instructions than two scalar tiles; the
+// per-lane arithmetic is the same, so results are identical).
+template <int NT, int M0, bool T0>
+__device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4& r, int kenter, int wsm, int kt,
+                                          int k0, float kt0f, TapGeo& g0, TapGeo& g1) {
+  const int ka = k0 + m * kTileK + kt;
+  const bool mem0 = !(m < M0 + tile_gran(NT)) || ka >= kenter;
+  const bool mem1 = !(m + 1 < M0 + tile_gran(NT)) || ka + kTileK >= kenter;
+  const float2 kf = make_float2(kt0f + (float)(m * kTileK), kt0f + (float)((m + 1) * kTileK));
+  const float2 h = __fmul2_rn(kf, make_float2(0.5f, 0.5f));
+  float2 h2 = __fmul2_rn(h, h);
+  if (m == 0 && ka == 0) h2.x = 1e-20f;
+  float2 delta = split_delay2(r.x, r.y, h, h2);
+  if (T0) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));
+  const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
+  const int idx0 = __float_as_int(tf.x) - wsm + m * kTileK;
+  const int idx1 = __float_as_int(tf.y) - wsm + (m + 1) * kTileK;
+  const float2 fr = sub2(delta, sub2(tf, make_float2(kFloorMagic, kFloorMagic)));
+  const float2 u = __fmul2_rn(make_float2(r.z, r.z),
+                              make_float2(rcp_ftz(fmaxf(kf.x, 1.f)), rcp_ftz(fmaxf(kf.y, 1.f))));
+  float2 w = __ffma2_rn(make_float2(__cosf(u.x), __cosf(u.y)), make_float2(a.win_b, a.win_b),
+                        make_float2(a.win_a, a.win_a));
+  w.x = mem0 ? w.x : 0.f;
+  w.y = mem1 ? w.y : 0.f;
+  const float2 w1 = __fmul2_rn(w, fr);
+  const float2 w0 = sub2(w, w1);
+  g0 = TapGeo{mem0 ? idx0 : 0, w0.x, w1.x};
+  g1 = TapGeo{mem1 ? idx1 : 0, w0.y, w1.y};
+}
+
+// One aperture entry, output tiles M0 .. NT-1 of the pass (straight-line):
+// an odd first tile alone, then tile pairs (2i, 2i+1) in packed geometry.
 // kt0f = (float)(k0 + kt): the thread's first output sample in the pass.
 template <int FB, int NT, int M0, bool T0>
 __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, int kenter, int wsm,
                                             const unsigned short* st, int kt, int k0, float kt0f,
                                             Acc<FB, NT>& acc) {
-  constexpr int FR = (NT * 8 + 2) * kRowSamples;
-#pragma unroll
-  for (int m = M0; m < NT; m++) {
-    const int k = k0 + m * kTileK + kt;
-    // the warp's first member tile is >= M0 and k_enter < k0 + (M0 + gran) * 256,
-    // so only the first gran tiles can hold non-members.  Outputs k >= S
-    // are computed but never stored; their taps stay inside the window.
-    const bool first = m < M0 + tile_gran(NT);
-    const bool mem = !first || k >= kenter;
-    const float kf = kt0f + (float)(m * kTileK);
-    const float h = 0.5f * kf;
-    const float h2 = (m == 0 && k == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
-    float delta = split_delay(r.x, r.y, h, h2);
-    if (T0) delta += a.t0fs;
-    const float tf = __fadd_rd(delta, kFloorMagic);
-    int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - k0 - kt)
-    const float fr = delta - (tf - kFloorMagic);
-    idx = mem ? idx : 0;
-    // opaque copy: keeps one materialised index so the 2 FB loads below use
-    // immediate offsets instead of one address add each
-    asm("mov.b32 %0, %0;" : "+r"(idx));
-    float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
-    w = mem ? w : 0.f;
-    // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
-    const float w1 = w * fr, w0 = w - w1;
-    const uint32_t pa = smem_u32(st) + 2u * (uint32_t)idx;
+  if constexpr (M0 & 1) {
+    const TapGeo g = tile_geo<NT, M0, T0>(M0, a, r, kenter, wsm, kt, k0, kt0f);
     if constexpr (FB == 1) {
-      acc.s[m] = fmaf(w0, lds_s16f(pa, 0), acc.s[m]);
-      acc.s[m] = fmaf(w1, lds_s16f(pa, 2), acc.s[m]);
+      const uint32_t pa = smem_u32(st) + 2u * (uint32_t)g.idx;
+      float& s1 = acc.s2[M0 / 2].y;
+      s1 = fmaf(g.w0, lds_s16f(pa, 0), s1);
+      s1 = fmaf(g.w1, lds_s16f(pa, 2), s1);
     } else {
+      tile_accumulate<FB, NT>(g, st, acc.p[M0]);
+    }
+  }
 #pragma unroll
-      for (int q = 0; q < FB / 2; q++) {
-        // sign-extending 16-bit loads + int->float (I2FP), packed over a frame pair
-        const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
-        const float2 x1 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR + 2), lds_s16f(pa, 2 * (2 * q + 1) * FR + 2));
-        acc.p[m][q] = __ffma2_rn(make_float2(w0, w0), x0, acc.p[m][q]);
-        acc.p[m][q] = __ffma2_rn(make_float2(w1, w1), x1, acc.p[m][q]);
-      }
+  for (int m = (M0 + 1) & ~1; m < NT; m += 2) {
+    TapGeo g0, g1;
+    tile_geo2<NT, M0, T0>(m, a, r, kenter, wsm, kt, k0, kt0f, g0, g1);
+    if constexpr (FB == 1) {
+      const uint32_t p0 = smem_u32(st) + 2u * (uint32_t)g0.idx, p1 = smem_u32(st) + 2u * (uint32_t)g1.idx;
+      const float2 x0 = make_float2(lds_s16f(p0, 0), lds_s16f(p1, 0));
+      const float2 x1 = make_float2(lds_s16f(p0, 2), lds_s16f(p1, 2));
+      acc.s2[m / 2] = __ffma2_rn(make_float2(g0.w0, g1.w0), x0, acc.s2[m / 2]);
+      acc.s2[m / 2] = __ffma2_rn(make_float2(g0.w1, g1.w1), x1, acc.s2[m / 2]);
+    } else {
+      tile_accumulate<FB, NT>(g0, st, acc.p[m]);
+      tile_accumulate<FB, NT>(g1, st, acc.p[m + 1]);
     }
   }
 }
@@ -344,7 +449,7 @@ __device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const fl
 }
 
 template <int FB, int NT, bool T0>
-__global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const DasArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int PL = NT * kTileK;                 // samples per pass
@@ -478,7 +583,7 @@ __global__ void __launch_bounds__(256, 2) das_fused_kernel(const __grid_constant
         const int n = (int)ncount[k];
         const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
         if constexpr (FB == 1) {
-          v[0] = acc.s[m] * inv;
+          v[0] = acc.s(m) * inv;
         } else {
 #pragma unroll
           for (int q = 0; q < FB / 2; q++) {
@@ -567,13 +672,17 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps) {
                                 {2, 8},  {2, 4}, {1, 16}, {1, 8}, {1, 4}};
   const int ntmax = das_nt(S);
   const int P = (fir_taps - 1) / 2;
-  for (auto& c : cand) {
-    const int fb = c[0], nt = c[1];
+  // dev override (A/B measurements): SUPRA_BF_SHAPE=<fb>x<nt>
+  int ofb = 0, ont = 0;
+  if (const char* ev = std::getenv("SUPRA_BF_SHAPE")) std::sscanf(ev, "%dx%d", &ofb, &ont);
+  for (int ci = -1; ci < (int)(sizeof cand / sizeof cand[0]); ci++) {
+    const int fb = ci < 0 ? ofb : cand[ci][0], nt = ci < 0 ? ont : cand[ci][1];
+    if (ci < 0 && !((fb == 16 && (nt == 2 || nt == 4)) || (fb == 8 && (nt == 2 || nt == 4 || nt == 8)))) continue;
     if (fb > fb_max || (fb > F && fb > 1) || nt > ntmax) continue;
     const size_t fixed = fixed_bytes(fb, nent_max, P);
     const size_t ring = 3 * stage_bytes(fb, das_rows_nt(nt));
     const size_t fir = align128((size_t)fir_groups(fb) * fir_span(nt * kTileK, P) * 16);
-    if (fixed + (ring > fir ? ring : fir) > kSmemBudget) continue;
+    if (fixed + (ring > fir ? ring : fir) > das_smem_budget(nt)) continue;
     return DasShape{fb, nt};
   }
   return DasShape{1, 4};
@@ -602,8 +711,10 @@ template <bool T0>
 static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, DasShape sh, cudaStream_t st) {
   const int nt = sh.nt;
   switch (sh.fb) {
-    case 16: return launch_k<16, 4, T0>(tm, a, st);
-    case 8: return nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st);
+    case 16: return nt == 2 ? launch_k<16, 2, T0>(tm, a, st) : launch_k<16, 4, T0>(tm, a, st);
+    case 8:
+      return nt == 2 ? launch_k<8, 2, T0>(tm, a, st)
+                     : (nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st));
     case 4:
       return nt == 4 ? launch_k<4, 4, T0>(tm, a, st)
                      : (nt == 8 ? launch_k<4, 8, T0>(tm, a, st) : launch_k<4, 16, T0>(tm, a, st));
