@@ -13,9 +13,9 @@ OUT = os.path.join(HERE, "libsupra_bf.so")
 BUILD = os.path.join(HERE, "_build")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["das.cu", "epilogue.cu", "scanconv.cu"]
+CU = ["das.cu", "das_warp.cu", "epilogue.cu", "scanconv.cu"]
 CPP = ["host.cpp"]
-HDRS = ["internal.h", "epilogue.cuh"]
+HDRS = ["internal.h", "epilogue.cuh", "das_common.cuh"]
 
 
 def _run(cmd, verbose):

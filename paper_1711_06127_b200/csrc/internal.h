@@ -172,6 +172,10 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // rows, C, E, F} with box {16, das_rows_nt(nt), 1, 1, fb} for sh = das_shape().
 cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, DasShape sh, cudaStream_t st);
 DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps);
+// One frame per CTA (fb = 1) with the aperture split across warps
+// (das_warp.cu); same tensor map as launch_das for that shape.
+bool das_warp_ok(int fb, int S, float t0fs);
+cudaError_t launch_das_warp(const CUtensorMap& raw_map, const DasArgs& a, cudaStream_t st);
 size_t das_smem_bytes(int fb, int nt, int nent_max, int fir_taps);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);

@@ -125,9 +125,15 @@ def test_c2_batch_parity_and_batch_invariance():
         e_rf, e_db, _, _ = check_frame(w, raw[f].cpu().numpy(), rf_g[f], y_g[f])
         assert e_rf <= RF_TOL, (f, e_rf)
         assert e_db <= DB_TOL, (f, e_db)
-    # frames are independent: one-at-a-time gives bitwise the same result
+    # frames are independent: any multi-frame batch gives bitwise the same
+    # result (one sum order per configuration) ...
+    rf2, y2 = run_gpu(bf, raw[4:6], 2)
+    assert np.array_equal(rf2[1], rf_g[5]) and np.array_equal(y2[1], y_g[5])
+    # ... and a single frame (the warp-split kernel, its own sum order)
+    # agrees to float32 rounding
     rf1, y1 = run_gpu(bf, raw[5:6], 1)
-    assert np.array_equal(rf1[0], rf_g[5]) and np.array_equal(y1[0], y_g[5])
+    assert rf_err(rf1[0], rf_g[5].astype(np.float64)) <= 1e-6
+    assert db_err(y1[0], y_g[5].astype(np.float64)) <= 1e-4
     # determinism
     rf_b, y_b = run_gpu(bf, raw, F)
     assert np.array_equal(rf_b, rf_g) and np.array_equal(y_b, y_g)
