@@ -40,7 +40,8 @@
 extern "C" {
 #endif
 
-#define SUPRA_BF_ABI_VERSION 1
+#define SUPRA_BF_ABI_VERSION 2
+#define SUPRA_MAX_BANDS 4   /* frequency-compounding bands */
 
 typedef struct supra_bf *supra_bf_t;
 
@@ -115,6 +116,18 @@ typedef struct {
     double out_origin_mm[3], out_spacing_mm[3];/* pixel (ix,iy,iz) at origin + i*spacing */
     double fov_x_deg, fov_y_deg;
     int32_t max_frames_per_call;               /* sizes the per-frame scratch */
+    /* frequency compounding through a bank of band-passes ("frequency
+     * compounding through a bank of configurable bandpasses"; S:186-189,
+     * S:210-218).  num_bands = 0: the single band (demod_frequency_hz,
+     * demod_bandwidth_hz), weight 1.  num_bands = 1..SUPRA_MAX_BANDS: band b
+     * demodulates at band_center_hz[b] with cutoff band_bandwidth_hz[b]/2
+     * (same fir_taps and decimation for every band, so outputs align), and
+     * env = sum_b band_weight[b] env_b.  Each band must lie inside (0, fs/2);
+     * weights >= 0 and sum to 1 within 1e-9; else SUPRA_E_PARAM. */
+    int32_t num_bands;
+    double band_center_hz[SUPRA_MAX_BANDS];
+    double band_bandwidth_hz[SUPRA_MAX_BANDS];
+    double band_weight[SUPRA_MAX_BANDS];
 } supra_bf_config;
 
 /*
@@ -139,7 +152,9 @@ supra_status supra_bf_create(const supra_bf_config *cfg, supra_bf_t *out);
  *   RF[l][k] = sum_{e : (2F) rho_le <= z} w(rho_le/R) x~_{ev(l),e}(tau_le(k)) / N
  *   tau = (z + |o_l + z d_l - pos_e|) fs/c + t0 fs, linear interpolation,
  *   zero outside [0, S) (reading #10), R = z/(2F), N = #members (0 -> 0).
- *   env[k] = 2 |sum_{j=-P..P} h_j RF[k-j] e^{-i w (k-j)}|  (w = 2 pi f_d / fs)
+ *   env[k] = 2 |sum_{j=-P..P} h_j RF[k-j] e^{-i w (k-j)}|  (w = 2 pi f_d / fs);
+ *   with a band bank env[k] = sum_b weight_b env_b[k], env_b the same with
+ *   (h^b, w_b) of band b (frequency compounding),
  *   y = 0 if env = 0, else clamp((20 log10(env/ref) + DR)/DR, 0, 1),
  *   ref = per-frame max of env (SUPRA_REF_FRAME_MAX) or reference_value.
  * Arguments:

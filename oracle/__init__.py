@@ -74,6 +74,8 @@ def lib():
         L.ora_iq_envelope.argtypes = [dp, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                       C.c_int, dp]
         L.ora_iq_envelope.restype = C.c_int
+        L.ora_compound.argtypes = [dp, C.c_int, C.c_double, C.c_int, dp, dp, dp, C.c_int, C.c_int, dp]
+        L.ora_compound.restype = C.c_int
         L.ora_log_compress.argtypes = [dp, C.c_long, C.c_int, C.c_double, C.c_double, dp]
         L.ora_log_compress.restype = C.c_double
         L.ora_to_u8.argtypes = [dp, C.c_long, C.c_void_p]
@@ -153,6 +155,36 @@ def iq_envelope(rf, fs_hz, fd_hz, bw_hz, taps=65, decimation=1):
     return out.reshape(shp[:-1] + (S // decimation,))
 
 
+def compound(rf, fs_hz, bands, taps=65, decimation=1):
+    """Frequency-compounded envelope: sum_b w_b * IQ envelope
+    of band b, bands = ((center Hz, bandwidth Hz, weight), ...); rf [..., S]."""
+    rf = np.ascontiguousarray(rf, np.float64)
+    shp = rf.shape
+    S = shp[-1]
+    flat = rf.reshape(-1, S)
+    fd = np.ascontiguousarray([b[0] for b in bands], np.float64)
+    bw = np.ascontiguousarray([b[1] for b in bands], np.float64)
+    wt = np.ascontiguousarray([b[2] for b in bands], np.float64)
+    out = np.zeros((flat.shape[0], S // decimation), np.float64)
+    for i in range(flat.shape[0]):
+        row = np.ascontiguousarray(flat[i])
+        o = np.zeros(S // decimation, np.float64)
+        rc = lib().ora_compound(_dptr(row), S, fs_hz, len(bands), _dptr(fd), _dptr(bw), _dptr(wt),
+                                taps, decimation, _dptr(o))
+        assert rc == 0
+        out[i] = o
+    return out.reshape(shp[:-1] + (S // decimation,))
+
+
+def envelope(cfg, rf):
+    """The envelope step a workload configures: compounding when cfg.bands is
+    set, else the single IQ band (demod_frequency, demod_bandwidth)."""
+    if getattr(cfg, "bands", ()):
+        return compound(rf, cfg.fs_hz, cfg.bands, cfg.fir_taps, cfg.decimation)
+    return iq_envelope(rf, cfg.fs_hz, cfg.demod_frequency_hz, cfg.demod_bandwidth_hz,
+                       cfg.fir_taps, cfg.decimation)
+
+
 def hilbert_envelope(x):
     """|analytic signal| by the DFT method: zero negative
     frequencies, double positive ones, keep DC and Nyquist, inverse DFT,
@@ -222,7 +254,6 @@ def scan_convert(cfg, line_img):
 def bmode_frame(cfg, raw, nthreads=None):
     """Whole oracle chain for one frame: (rf, env, y_line, ref)."""
     rf = das(cfg, raw, nthreads=nthreads)
-    env = iq_envelope(rf, cfg.fs_hz, cfg.demod_frequency_hz, cfg.demod_bandwidth_hz,
-                      cfg.fir_taps, cfg.decimation)
+    env = envelope(cfg, rf)
     y, ref = log_compress(env, cfg.dynamic_range_db, cfg.reference_mode, cfg.reference_value)
     return rf, env, y, ref

@@ -228,6 +228,28 @@ int ora_iq_envelope(const double *rf, int S, double fs_hz, double fd_hz, double 
     return 0;
 }
 
+/* Frequency compounding through a bank of band-passes ("frequency
+ * compounding through a bank of configurable bandpasses"; S:186-189 the
+ * BandpassBank, "weighted sum of per-band iq_demodulate outputs; all
+ * bands share one decimation factor so outputs align sample-for-sample"):
+ *   env[q] = sum_{b=0}^{nb-1} w_b env_b[q],  env_b = ora_iq_envelope(rf, band b).
+ * Bands are summed in order b = 0, 1, ...                                 */
+int ora_compound(const double *rf, int S, double fs_hz, int nb, const double *fd_hz,
+                 const double *bw_hz, const double *w, int T, int dec, double *env)
+{
+    if (nb < 1 || dec < 1) return -1;
+    int nout = S / dec;
+    double *eb = (double *)malloc(sizeof(double) * (size_t)(nout > 0 ? nout : 1));
+    if (!eb) return -1;
+    for (int q = 0; q < nout; q++) env[q] = 0.0;
+    for (int b = 0; b < nb; b++) {
+        if (ora_iq_envelope(rf, S, fs_hz, fd_hz[b], bw_hz[b], T, dec, eb) != 0) { free(eb); return -1; }
+        for (int q = 0; q < nout; q++) env[q] += w[b] * eb[q];
+    }
+    free(eb);
+    return 0;
+}
+
 /* Log compression:
  *   y = 0 if x = 0, else clamp((20 log10(x/ref) + DR)/DR, 0, 1).
  * ref_mode 0: ref = max over the n values given (the frame);

@@ -18,7 +18,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # (A/B measurements of kernel variants); the default is the in-tree build.
 LIB_PATH = os.environ.get("SUPRA_BF_LIB") or os.path.join(HERE, "libsupra_bf.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
+MAX_BANDS = 4
 OK, E_PARAM, E_STRUCT, E_RESOURCE, E_CUDA = 0, 2, 3, 4, 5
 WIN_RECT, WIN_HANN, WIN_HAMMING = 0, 1, 2
 NORM_COUNT, NORM_NONE = 0, 1
@@ -61,6 +62,9 @@ class Config(C.Structure):
         ("out_origin_mm", C.c_double * 3), ("out_spacing_mm", C.c_double * 3),
         ("fov_x_deg", C.c_double), ("fov_y_deg", C.c_double),
         ("max_frames_per_call", C.c_int32),
+        ("num_bands", C.c_int32),
+        ("band_center_hz", C.c_double * MAX_BANDS), ("band_bandwidth_hz", C.c_double * MAX_BANDS),
+        ("band_weight", C.c_double * MAX_BANDS),
     ]
 
 
@@ -136,6 +140,12 @@ def make_config(w, device: int = 0, max_frames: int = 1, **over) -> tuple:
     c.out_spacing_mm = (C.c_double * 3)(*w.out_spacing_mm)
     c.fov_x_deg, c.fov_y_deg = w.fov_x_deg, w.fov_y_deg
     c.max_frames_per_call = max_frames
+    bands = list(getattr(w, "bands", ()) or ())
+    if len(bands) > MAX_BANDS:
+        raise ValueError(f"at most {MAX_BANDS} compounding bands")
+    c.num_bands = len(bands)
+    for b, (fc, bw, wt) in enumerate(bands):
+        c.band_center_hz[b], c.band_bandwidth_hz[b], c.band_weight[b] = fc, bw, wt
     for k, v in over.items():
         setattr(c, k, v)
     return c, (org, dirs, ev)

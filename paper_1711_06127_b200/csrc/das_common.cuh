@@ -144,17 +144,19 @@ __host__ __device__ inline int fir_groups(int FB) { return (FB + 3) / 4; }
 // position b = k - kbase; RF outside [0, S) is zero in the buffer), then log
 // compression or env + running max.
 // b[k] = c0 x[k] + sum_{j>=1} c_j (x[k-j] + x[k+j]) + i s_j (x[k-j] - x[k+j])
-// (reading #18: g_j = h_j e^{+i w j}, h symmetric), env = 2 |b|.
-template <int FB>
-__device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int kbase, int o0, int o_end,
-                                          int line, int fg0, float* bmax) {
-  const int P = (a.fir_taps - 1) / 2;
+// (reading #18: g_j = h_j e^{+i w j}, h symmetric), env = 2 |b|; with a band
+// bank (frequency compounding) env = sum_b w_b env_b, bands in
+// order (the arithmetic of epilogue.cuh envelope_at, so fused and standalone
+// results agree bitwise).
+template <int B>
+__device__ __forceinline__ void band_env(const DasArgs& a, const float4* lineg, int kbase, int o0, int P,
+                                         float (&env)[4][4]) {
   auto X = [&](int k) { return lineg[fir_pad(k - kbase)]; };
   float4 Lw[4], Rw[4];
 #pragma unroll
   for (int o = 0; o < 4; o++) Lw[o] = Rw[o] = X(o0 + o);
   float2 re[4][2], im[4][2];
-  const float c0 = a.fir_c[0];
+  const float c0 = a.fir_c[B][0];
 #pragma unroll
   for (int o = 0; o < 4; o++) {
     re[o][0] = __fmul2_rn(make_float2(c0, c0), make_float2(Lw[o].x, Lw[o].y));
@@ -167,7 +169,7 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
     // shift: Lw[o] = x[o0 + o - j], Rw[o] = x[o0 + o + j]
     Lw[3] = Lw[2]; Lw[2] = Lw[1]; Lw[1] = Lw[0]; Lw[0] = X(o0 - j);
     Rw[0] = Rw[1]; Rw[1] = Rw[2]; Rw[2] = Rw[3]; Rw[3] = X(o0 + 3 + j);
-    const float2 cj = make_float2(a.fir_c[j], a.fir_c[j]), sj = make_float2(a.fir_s[j], a.fir_s[j]);
+    const float2 cj = make_float2(a.fir_c[B][j], a.fir_c[B][j]), sj = make_float2(a.fir_s[B][j], a.fir_s[B][j]);
 #pragma unroll
     for (int o = 0; o < 4; o++) {
       const float2 l0 = make_float2(Lw[o].x, Lw[o].y), l1 = make_float2(Lw[o].z, Lw[o].w);
@@ -178,31 +180,48 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
       im[o][1] = __ffma2_rn(sj, sub2(l1, r1), im[o][1]);
     }
   }
+  const float w = a.band_w[B];
+#pragma unroll
+  for (int o = 0; o < 4; o++) {
+    const float2 e0 = __ffma2_rn(re[o][0], re[o][0], __fmul2_rn(im[o][0], im[o][0]));
+    const float2 e1 = __ffma2_rn(re[o][1], re[o][1], __fmul2_rn(im[o][1], im[o][1]));
+    const float eb[4] = {2.f * sqrtf(e0.x), 2.f * sqrtf(e0.y), 2.f * sqrtf(e1.x), 2.f * sqrtf(e1.y)};
+#pragma unroll
+    for (int q = 0; q < 4; q++) env[o][q] = B == 0 ? w * eb[q] : fmaf(w, eb[q], env[o][q]);
+  }
+}
+
+template <int FB>
+__device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int kbase, int o0, int o_end,
+                                          int line, int fg0, float* bmax) {
+  const int P = (a.fir_taps - 1) / 2;
+  float env[4][4];
+  band_env<0>(a, lineg, kbase, o0, P, env);
+  if (a.nbands > 1) band_env<1>(a, lineg, kbase, o0, P, env);
+  if (a.nbands > 2) band_env<2>(a, lineg, kbase, o0, P, env);
+  if (a.nbands > 3) band_env<3>(a, lineg, kbase, o0, P, env);
+  static_assert(kMaxBands == 4, "band unrolling");
 #pragma unroll
   for (int o = 0; o < 4; o++) {
     const int k = o0 + o;
     if (k >= o_end) break;
-    const float2 e0 = __ffma2_rn(re[o][0], re[o][0], __fmul2_rn(im[o][0], im[o][0]));
-    const float2 e1 = __ffma2_rn(re[o][1], re[o][1], __fmul2_rn(im[o][1], im[o][1]));
-    const float env[4] = {2.f * sqrtf(e0.x), 2.f * sqrtf(e0.y), 2.f * sqrtf(e1.x), 2.f * sqrtf(e1.y)};
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const int f = fg0 + q;
       if (q >= FB || f >= a.F) break;
       const size_t out = ((size_t)f * a.L + line) * a.S + k;
+      const float e = env[o][q];
       if (a.ref_fixed) {
-        const float e = env[q];
         const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(e), a.log_k0), 0.f), 1.f) : 0.f;
         if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[out] = (uint8_t)floorf(255.f * y + 0.5f);
         else ((float*)a.y_out)[out] = y;
       } else {
-        a.env_out[out] = env[q];
-        bmax[q] = fmaxf(bmax[q], env[q]);
+        a.env_out[out] = e;
+        bmax[q] = fmaxf(bmax[q], e);
       }
     }
   }
 }
-
 
 }  // namespace
 }  // namespace supra

@@ -12,14 +12,15 @@ namespace supra {
 __global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int S = a.S, P = (a.fir_taps - 1) / 2;
-  float* cs = (float*)smem_raw;                  // c[0..P], s[0..P]
-  float* rfs = cs + 2 * (kMaxHalfTaps + 1);
+  float* cs = (float*)smem_raw;                  // per band: c[0..P], s[0..P]
+  float* rfs = cs + a.nbands * kCsRow;
   __shared__ unsigned smax;
   const int line = blockIdx.x, f = blockIdx.y;
   const float* src = a.rf + ((size_t)f * a.L + line) * S;
-  for (int i = threadIdx.x; i <= P; i += blockDim.x) {
-    cs[i] = a.fir[i + P].x;
-    cs[kMaxHalfTaps + 1 + i] = a.fir[i + P].y;
+  for (int i = threadIdx.x; i < a.nbands * (P + 1); i += blockDim.x) {
+    const int b = i / (P + 1), j = i - b * (P + 1);
+    cs[b * kCsRow + j] = a.fir[b * a.fir_taps + j + P].x;
+    cs[b * kCsRow + kMaxHalfTaps + 1 + j] = a.fir[b * a.fir_taps + j + P].y;
   }
   for (int i = threadIdx.x; i < S + 2 * P; i += blockDim.x) {
     int k = i - P;
@@ -29,7 +30,7 @@ __global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
   __syncthreads();
   float m = 0.f;
   for (int k = threadIdx.x; k < S; k += blockDim.x) {
-    const float env = envelope_at(rfs + P + k, cs, cs + kMaxHalfTaps + 1, P);
+    const float env = compound_at(rfs + P + k, cs, a.band_w, a.nbands, P);
     const size_t o = ((size_t)f * a.L + line) * S + k;
     if (a.ref_fixed) {
       const float y = env > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(env), a.log_k0), 0.f), 1.f) : 0.f;
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs a) {
 
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st) {
   const int P = (a.fir_taps - 1) / 2;
-  size_t smem = sizeof(float) * (2 * (kMaxHalfTaps + 1) + a.S + 2 * P);
+  size_t smem = sizeof(float) * (a.nbands * kCsRow + a.S + 2 * P);
   cudaError_t e = cudaFuncSetAttribute(envlog_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.L, a.F);

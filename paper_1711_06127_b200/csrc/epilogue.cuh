@@ -19,4 +19,13 @@ __device__ __forceinline__ float envelope_at(const float* x, const float* c, con
   return 2.f * sqrtf(fmaf(re, re, im * im));
 }
 
+// Band bank (frequency compounding): env = sum_b w_b env_b,
+// bands in order; cs holds [band][c 0..P | s 0..P] with row kCsRow.
+constexpr int kCsRow = 2 * (kMaxHalfTaps + 1);
+__device__ __forceinline__ float compound_at(const float* x, const float* cs, const float* w, int nb, int P) {
+  float env = w[0] * envelope_at(x, cs, cs + kMaxHalfTaps + 1, P);
+  for (int b = 1; b < nb; b++) env = fmaf(w[b], envelope_at(x, cs + b * kCsRow, cs + b * kCsRow + kMaxHalfTaps + 1, P), env);
+  return env;
+}
+
 }  // namespace supra

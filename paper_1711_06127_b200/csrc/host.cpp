@@ -84,7 +84,9 @@ struct supra_bf {
   std::vector<ScAxis> h_ax, h_az;
   std::vector<ScRow> h_rows;
   std::vector<ScEntry> h_ent;
-  std::vector<float> fir_c, fir_s;
+  int nbands = 1;
+  float band_w[kMaxBands] = {1.f, 0.f, 0.f, 0.f};
+  std::vector<float> fir_c, fir_s;  // [kMaxBands][kMaxHalfTaps + 1]
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
   int64_t info[8] = {0};
 };
@@ -163,6 +165,18 @@ supra_status validate(const supra_bf_config* c) {
   double fd = c->demod_frequency_hz, bw = c->demod_bandwidth_hz;
   if (!(bw > 0) || !(fd - bw / 2 > 0) || !(fd + bw / 2 < c->sample_frequency_hz / 2))
     return fail(SUPRA_E_PARAM, "demodulation band must lie inside (0, fs/2) (S:188)");
+  if (c->num_bands < 0 || c->num_bands > SUPRA_MAX_BANDS)
+    return fail(SUPRA_E_PARAM, "num_bands must be in [0, %d]", SUPRA_MAX_BANDS);
+  double wsum = 0.0;
+  for (int b = 0; b < c->num_bands; b++) {
+    const double bc = c->band_center_hz[b], bb = c->band_bandwidth_hz[b], bw_ = c->band_weight[b];
+    if (!(bb > 0) || !(bc - bb / 2 > 0) || !(bc + bb / 2 < c->sample_frequency_hz / 2))
+      return fail(SUPRA_E_PARAM, "band %d must lie inside (0, fs/2) (S:188)", b);
+    if (!(bw_ >= 0) || !std::isfinite(bw_)) return fail(SUPRA_E_PARAM, "band weight %d must be >= 0", b);
+    wsum += bw_;
+  }
+  if (c->num_bands > 0 && !(std::fabs(wsum - 1.0) <= 1e-9))
+    return fail(SUPRA_E_PARAM, "band weights must sum to 1 within 1e-9 (S:187)");
   if (!(c->dynamic_range_db > 0)) return fail(SUPRA_E_PARAM, "dynamic_range_db must be > 0 (S:247)");
   if (c->reference_mode != SUPRA_REF_FRAME_MAX && c->reference_mode != SUPRA_REF_FIXED)
     return fail(SUPRA_E_PARAM, "reference_mode");
@@ -305,30 +319,38 @@ supra_status build_das_tables(supra_bf* h) {
   for (int l = 0; l < L; l++)
     dirs[l] = make_float4((float)c.line_direction[3 * l], (float)c.line_direction[3 * l + 1],
                           (float)c.line_direction[3 * l + 2], 0.f);
-  // FIR: Hamming-windowed sinc low-pass, cutoff bw/2, DC gain 1 (S:227,
-  // reading #16), rotated to the complex band-pass g_j = h_j e^{+i w j}
-  // (reading #18), w = 2 pi f_d / fs.
+  // FIR per band: Hamming-windowed sinc low-pass, cutoff bw/2, DC gain 1
+  // (reading #16), rotated to the complex band-pass g_j = h_j e^{+i w j}
+  // (reading #18), w = 2 pi f_d / fs.  num_bands = 0: the single
+  // (demod_frequency, demod_bandwidth) band with weight 1; else the bank
+  // (frequency compounding).
   const int T = c.fir_taps, P = (T - 1) / 2;
-  const double fc = c.demod_bandwidth_hz / 2.0, fs = c.sample_frequency_hz;
-  std::vector<double> hd(T);
-  double sum = 0;
-  for (int j = -P; j <= P; j++) {
-    double s = (j == 0) ? 2.0 * fc / fs : std::sin(2.0 * kPi * fc * j / fs) / (kPi * j);
-    double w = (T > 1) ? 0.54 + 0.46 * std::cos(2.0 * kPi * j / (T - 1)) : 1.0;
-    hd[j + P] = w * s;
-    sum += w * s;
-  }
-  std::vector<float2> fir(T);
-  const double om = 2.0 * kPi * c.demod_frequency_hz / fs;
-  for (int j = -P; j <= P; j++) {
-    double hj = hd[j + P] / sum;
-    fir[j + P] = make_float2((float)(hj * std::cos(om * j)), (float)(hj * std::sin(om * j)));
-  }
-  h->fir_c.assign(kMaxHalfTaps + 1, 0.f);
-  h->fir_s.assign(kMaxHalfTaps + 1, 0.f);
-  for (int j = 0; j <= P; j++) {
-    h->fir_c[j] = fir[j + P].x;
-    h->fir_s[j] = fir[j + P].y;
+  const double fs = c.sample_frequency_hz;
+  h->nbands = c.num_bands > 0 ? c.num_bands : 1;
+  std::vector<float2> fir((size_t)h->nbands * T);
+  h->fir_c.assign((size_t)kMaxBands * (kMaxHalfTaps + 1), 0.f);
+  h->fir_s.assign((size_t)kMaxBands * (kMaxHalfTaps + 1), 0.f);
+  for (int b = 0; b < h->nbands; b++) {
+    const double fd = c.num_bands > 0 ? c.band_center_hz[b] : c.demod_frequency_hz;
+    const double fc = (c.num_bands > 0 ? c.band_bandwidth_hz[b] : c.demod_bandwidth_hz) / 2.0;
+    h->band_w[b] = c.num_bands > 0 ? (float)c.band_weight[b] : 1.0f;
+    std::vector<double> hd(T);
+    double sum = 0;
+    for (int j = -P; j <= P; j++) {
+      double s = (j == 0) ? 2.0 * fc / fs : std::sin(2.0 * kPi * fc * j / fs) / (kPi * j);
+      double w = (T > 1) ? 0.54 + 0.46 * std::cos(2.0 * kPi * j / (T - 1)) : 1.0;
+      hd[j + P] = w * s;
+      sum += w * s;
+    }
+    const double om = 2.0 * kPi * fd / fs;
+    for (int j = -P; j <= P; j++) {
+      double hj = hd[j + P] / sum;
+      fir[(size_t)b * T + j + P] = make_float2((float)(hj * std::cos(om * j)), (float)(hj * std::sin(om * j)));
+    }
+    for (int j = 0; j <= P; j++) {
+      h->fir_c[(size_t)b * (kMaxHalfTaps + 1) + j] = fir[(size_t)b * T + j + P].x;
+      h->fir_s[(size_t)b * (kMaxHalfTaps + 1) + j] = fir[(size_t)b * T + j + P].y;
+    }
   }
   cudaError_t e;
   if ((e = upload(&h->d_line_group, line_group)) != cudaSuccess ||
@@ -689,9 +711,13 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.debug_skip = std::getenv("SUPRA_BF_DEBUG") ? std::atoi(std::getenv("SUPRA_BF_DEBUG")) : 0;
   a.fir = h->d_fir;
   a.fir_taps = c.fir_taps;
-  for (int j = 0; j <= kMaxHalfTaps; j++) {
-    a.fir_c[j] = h->fir_c[j];
-    a.fir_s[j] = h->fir_s[j];
+  a.nbands = h->nbands;
+  for (int b = 0; b < kMaxBands; b++) {
+    a.band_w[b] = h->band_w[b];
+    for (int j = 0; j <= kMaxHalfTaps; j++) {
+      a.fir_c[b][j] = h->fir_c[(size_t)b * (kMaxHalfTaps + 1) + j];
+      a.fir_s[b][j] = h->fir_s[(size_t)b * (kMaxHalfTaps + 1) + j];
+    }
   }
   fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
   a.y_type = c.line_output_type;
@@ -856,6 +882,8 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames
   a.S = h->S;
   a.fir = h->d_fir;
   a.fir_taps = c.fir_taps;
+  a.nbands = h->nbands;
+  for (int b = 0; b < kMaxBands; b++) a.band_w[b] = h->band_w[b];
   fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
   a.y_type = c.line_output_type;
   if (a.ref_fixed) {

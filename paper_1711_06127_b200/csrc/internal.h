@@ -19,6 +19,8 @@ constexpr int kRowSamples = 32;
 constexpr int kMaxStages = 8;
 // FIR half-length limit (fir_taps <= 2*kMaxHalfTaps + 1 = 129).
 constexpr int kMaxHalfTaps = 64;
+// Frequency-compounding bands (SUPRA_MAX_BANDS).
+constexpr int kMaxBands = SUPRA_MAX_BANDS;
 // Largest record the DAS kernel holds per line (NT = 16 tiles).
 constexpr int kMaxSamples = 16 * kTileK;
 // Output tiles per thread and pass (a template parameter of the DAS kernel,
@@ -66,14 +68,16 @@ struct DasArgs {
   // outputs
   float* rf;                   // [F][L][S] or null
   int do_epilogue;             // 1: FIR + envelope (+ log) epilogue
-  const float2* fir;           // [T] complex taps g_j = h_j e^{+i w j}, j = -P..P
+  const float2* fir;           // [nbands][T] complex taps g_j = h_j e^{+i w j}, j = -P..P
   int fir_taps;
   // the same taps split by symmetry (reading #18): c_j = Re g_j (even),
-  // s_j = Im g_{-j} = -Im g_j ... stored for j = 0..P as c[j] = Re g_j,
-  // s[j] = Im g_j; passed by value so the unrolled FIR reads them from the
-  // constant bank (uniform-register operands of FFMA2).
-  float fir_c[kMaxHalfTaps + 1];
-  float fir_s[kMaxHalfTaps + 1];
+  // s_j = Im g_{-j} = -Im g_j ... stored for j = 0..P as c[b][j] = Re g_j,
+  // s[b][j] = Im g_j of band b; passed by value so the unrolled FIR reads
+  // them from the constant bank (uniform-register operands of FFMA2).
+  int nbands;                  // 1 .. kMaxBands (frequency compounding)
+  float band_w[kMaxBands];     // env = sum_b band_w[b] env_b
+  float fir_c[kMaxBands][kMaxHalfTaps + 1];
+  float fir_s[kMaxBands][kMaxHalfTaps + 1];
   int ref_fixed;               // 1: y written directly; 0: env written + frame max
   float log_k1, log_k0;        // y = k1 log2(env) + k0 (fixed reference)
   float* env_out;              // [F][L][S] f32 (frame-max mode)
@@ -86,8 +90,10 @@ struct DasArgs {
 struct EnvArgs {  // standalone epilogue on an RF buffer
   const float* rf;
   int F, L, S;
-  const float2* fir;
+  const float2* fir;   // [nbands][T]
   int fir_taps;
+  int nbands;
+  float band_w[kMaxBands];
   int ref_fixed;
   float log_k1, log_k0;
   float* env_out;

@@ -64,6 +64,9 @@ class Workload:
     demod_bandwidth_hz: float = 0.0     # default: 0.6 f0
     fir_taps: int = 65
     decimation: int = 1
+    # frequency compounding: ((center Hz, bandwidth Hz,
+    # weight), ...); empty = the single (demod_frequency, demod_bandwidth) band
+    bands: tuple = ()
     dynamic_range_db: float = 50.0
     reference_mode: int = REF_FRAME_MAX
     reference_value: float = 1.0

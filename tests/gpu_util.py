@@ -45,5 +45,5 @@ def run_gpu(bf, raw, frames, want_rf=True):
 
 def oracle_chain(w, raw_np, lines=None, nthreads=None):
     rf = oracle.das(w, raw_np, lines=lines, nthreads=nthreads)
-    env = oracle.iq_envelope(rf, w.fs_hz, w.demod_frequency_hz, w.demod_bandwidth_hz, w.fir_taps)
+    env = oracle.envelope(w, rf)
     return rf, env

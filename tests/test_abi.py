@@ -121,3 +121,23 @@ def test_null_handle_calls():
     assert L.supra_bf_scanconvert(None, None, 1, None, None, None) == binding.E_STRUCT
     L.supra_bf_destroy(None)
     assert _create.__name__  # destroy(NULL) is a no-op
+
+
+@pytest.mark.parametrize("bands", [
+    ((7e6, 4.2e6, 0.5), (3.5e6, 2e6, 0.4)),        # weights sum to 0.9
+    ((7e6, 4.2e6, 1.2), (3.5e6, 2e6, -0.2)),       # negative weight
+    ((7e6, 4.2e6, 0.5), (19.5e6, 2e6, 0.5)),       # band past fs/2
+    ((7e6, 4.2e6, 0.2),) * 5,                      # more than SUPRA_MAX_BANDS
+])
+def test_band_bank_errors(bands):
+    w = configs.c1(bands=bands)
+    if len(bands) > binding.MAX_BANDS:
+        with pytest.raises(ValueError):
+            binding.make_config(w)
+        cfg, _ = binding.make_config(configs.c1(bands=bands[:4]))
+        cfg.num_bands = 5
+        h = C.c_void_p()
+        assert binding.lib().supra_bf_create(C.byref(cfg), C.byref(h)) == binding.E_PARAM
+        return
+    rc, msg = _create(w)
+    assert rc == binding.E_PARAM and "band" in msg, (rc, msg)

@@ -122,3 +122,75 @@ def test_log_frame_max_scale_invariance_S263():
 def test_log_all_zero_frame():
     y, ref = oracle.log_compress(np.zeros(100), 50.0)
     assert ref == 0.0 and np.all(y == 0.0)
+
+
+# ------------------------------------------------- frequency compounding
+# P:121 "frequency compounding through a bank of configurable bandpasses";
+# S:186-189 (BandpassBank), S:213-218 (compound and its examples).
+FS = 40e6
+BAND_LO = (3.0e6, 2.0e6)      # 2 .. 4 MHz
+BAND_HI = (8.0e6, 2.0e6)      # 7 .. 9 MHz (disjoint, equal widths)
+
+
+def _tone(f, A, N=4096):
+    n = np.arange(N)
+    return A * np.cos(2 * np.pi * f * n / FS + 0.3)
+
+
+def test_compound_single_band_weight_one_is_iq_demodulate():
+    # single band, weight 1 -> identical to iq_demodulate
+    x = np.random.default_rng(3).standard_normal(2048)
+    e1 = oracle.compound(x, FS, ((7e6, 4.2e6, 1.0),))
+    e2 = oracle.iq_envelope(x, FS, 7e6, 4.2e6)
+    assert np.array_equal(e1, e2)
+
+
+@pytest.mark.parametrize("wlo", [0.5, 0.3, 0.8])
+def test_compound_tone_inside_one_band(wlo):
+    # two disjoint bands, tone inside band 1 only -> w1 x single-band
+    # envelope within 2% (band 2 rejects it below -40 dB); here the
+    # single-band envelope of a tone of amplitude A is A, so the
+    # closed form is w1 A.
+    bands = ((*BAND_LO, wlo), (*BAND_HI, 1.0 - wlo))
+    A = 1.7
+    mid = slice(200, -200)
+    e = oracle.compound(_tone(3.0e6, A), FS, bands)[mid]
+    assert np.max(np.abs(e - wlo * A)) <= 0.02 * wlo * A
+    e = oracle.compound(_tone(8.0e6, A), FS, bands)[mid]
+    assert np.max(np.abs(e - (1 - wlo) * A)) <= 0.02 * (1 - wlo) * A
+
+
+def test_compound_two_tones_one_per_band():
+    # superposition across disjoint bands: w1 A1 + w2 A2 within 2%
+    bands = ((*BAND_LO, 0.4), (*BAND_HI, 0.6))
+    x = _tone(3.0e6, 2.0) + _tone(8.0e6, 0.5)
+    e = oracle.compound(x, FS, bands)[200:-200]
+    want = 0.4 * 2.0 + 0.6 * 0.5
+    assert np.max(np.abs(e - want)) <= 0.02 * want
+
+
+def test_compound_scale_equivariance_and_sign():
+    # envelope(a x) = a envelope(x), envelope(-x) = envelope(x)
+    bands = ((*BAND_LO, 0.5), (*BAND_HI, 0.5))
+    x = np.random.default_rng(5).standard_normal(1024)
+    e = oracle.compound(x, FS, bands)
+    assert np.allclose(oracle.compound(3.5 * x, FS, bands), 3.5 * e, rtol=1e-12, atol=0)
+    assert np.allclose(oracle.compound(-x, FS, bands), e, rtol=1e-12, atol=0)
+
+
+def test_compound_reduces_speckle_variance():
+    # uniform white-noise input -> the compounded envelope's variance
+    # is <= the minimum single-band variance (speckle reduction), over >= 100
+    # realisations.  With equal weights and disjoint equal-width bands the
+    # band envelopes are independent, so the variance halves (bound: <= min).
+    rng = np.random.default_rng(11)
+    bands = ((*BAND_LO, 0.5), (*BAND_HI, 0.5))
+    vc = vl = vh = 0.0
+    R = 100
+    for _ in range(R):
+        x = rng.standard_normal(1024)
+        vc += np.var(oracle.compound(x, FS, bands)[100:-100])
+        vl += np.var(oracle.iq_envelope(x, FS, *BAND_LO)[100:-100])
+        vh += np.var(oracle.iq_envelope(x, FS, *BAND_HI)[100:-100])
+    assert vc / R <= min(vl, vh) / R
+    assert vc / R <= 0.7 * min(vl, vh) / R      # and clearly so (~0.5)
