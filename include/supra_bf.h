@@ -128,6 +128,18 @@ typedef struct {
     double band_center_hz[SUPRA_MAX_BANDS];
     double band_bandwidth_hz[SUPRA_MAX_BANDS];
     double band_weight[SUPRA_MAX_BANDS];
+    /* receive channel map (the 128-element probe of Table 1 with only
+     * 64 usable channels; "an active-aperture width parameter").
+     * num_channels = 0: one channel per element, ch = j*Nx + i (reading #15),
+     * raw frames [num_events][Nx*Ny][samples].  num_channels >= 1: raw frames
+     * are [num_events][num_channels][samples] and channel_element
+     * [num_events][num_channels] gives the element channel ch of event e
+     * recorded (-1: unused).  The receive aperture of a line is the set of
+     * elements its event recorded; N(k) counts only those (reading #7).
+     * An element listed twice in one event, or outside [-1, Nx*Ny), is
+     * SUPRA_E_STRUCT. */
+    int32_t num_channels;
+    const int32_t *channel_element;
 } supra_bf_config;
 
 /*
@@ -159,6 +171,7 @@ supra_status supra_bf_create(const supra_bf_config *cfg, supra_bf_t *out);
  *   ref = per-frame max of env (SUPRA_REF_FRAME_MAX) or reference_value.
  * Arguments:
  *   raw      : device, int16 [frames][num_events][channels][samples], 16-byte aligned
+ *              (channels = num_channels, or Nx*Ny when num_channels = 0)
  *              (read through a TMA tensor map encoded per call).
  *   frames   : 0 .. max_frames_per_call (0 = no-op).
  *   rf       : device float [frames][L][samples] or NULL.

@@ -43,7 +43,8 @@ class _DasParams(C.Structure):
                 ("L", C.c_int),
                 ("origin_mm", C.POINTER(C.c_double)), ("direction", C.POINTER(C.c_double)),
                 ("line_event", C.POINTER(C.c_int32)),
-                ("f_number", C.c_double), ("window", C.c_int), ("normalize", C.c_int)]
+                ("f_number", C.c_double), ("window", C.c_int), ("normalize", C.c_int),
+                ("nch", C.c_int), ("chmap", C.POINTER(C.c_int32))]
 
 
 class _ScParams(C.Structure):
@@ -113,7 +114,11 @@ def das(cfg, raw, lines=None, nthreads=None):
     attributes); ``lines`` selects a subset of scanlines (default: all)."""
     raw = np.ascontiguousarray(raw, np.int16)
     E, Cc, S = raw.shape
-    assert E == cfg.num_events and Cc == cfg.elements_x * cfg.elements_y and S == cfg.S
+    chmap = getattr(cfg, "channel_element", None)
+    nch = 0 if chmap is None else int(np.shape(chmap)[1])
+    chmap = None if chmap is None else np.ascontiguousarray(chmap, np.int32)
+    assert E == cfg.num_events and S == cfg.S
+    assert Cc == (nch if nch else cfg.elements_x * cfg.elements_y)
     org = np.ascontiguousarray(cfg.line_origin_mm, np.float64)
     dirs = np.ascontiguousarray(cfg.line_direction, np.float64)
     ev = np.ascontiguousarray(cfg.line_event, np.int32)
@@ -124,7 +129,8 @@ def das(cfg, raw, lines=None, nthreads=None):
     p = _DasParams(cfg.elements_x, cfg.elements_y, cfg.pitch_x_mm, cfg.pitch_y_mm, E, S,
                    cfg.fs_hz, cfg.c_mps, cfg.t0_s, L, _dptr(org), _dptr(dirs),
                    ev.ctypes.data_as(C.POINTER(C.c_int32)), cfg.f_number, cfg.window,
-                   cfg.normalize)
+                   cfg.normalize, nch,
+                   None if chmap is None else chmap.ctypes.data_as(C.POINTER(C.c_int32)))
     rf = np.zeros((len(lines), S), np.float64)
     nt = nthreads or min(len(lines), os.cpu_count() or 1)
     rc = lib().ora_das(C.byref(p), raw.ctypes.data, lines.ctypes.data, len(lines), _dptr(rf),

@@ -92,6 +92,13 @@ typedef struct {
     const int32_t *line_event; /* [L]    */
     double f_number;
     int window, normalize;
+    /* receive channel map ("only 64 channels usable"; S:102 active
+     * aperture): nch = 0 -> channel ch is element ch; else raw holds nch
+     * traces per event and chmap[ev*nch + ch] is the element channel ch
+     * recorded (-1: unused).  The receive aperture of a line is the set of
+     * elements its event recorded.                                       */
+    int nch;
+    const int32_t *chmap;
 } ora_das_params;
 
 /* Delay-and-sum with dynamic receive focusing (S:133,
@@ -103,17 +110,20 @@ static void ora_das_line(const ora_das_params *p, const double *pos, const int16
                          int l, double *rf)
 {
     const double dr = 1000.0 * p->c_mps / (2.0 * p->fs_hz);
-    const int C = p->nx * p->ny;
+    const int C = p->nch > 0 ? p->nch : p->nx * p->ny;   /* traces per event */
     const int S = p->S;
     const double *o = p->origin_mm + 3 * l;
     const double *d = p->direction + 3 * l;
-    const int16_t *xev = raw + (size_t)p->line_event[l] * (size_t)C * (size_t)S;
+    const int ev = p->line_event[l];
+    const int16_t *xev = raw + (size_t)ev * (size_t)C * (size_t)S;
     for (int k = 0; k < S; k++) {
         double z = k * dr;
         double sum = 0.0;
         int n = 0;
         for (int ch = 0; ch < C; ch++) {
-            const double *e = pos + 3 * ch;
+            const int el = p->nch > 0 ? p->chmap[(size_t)ev * p->nch + ch] : ch;
+            if (el < 0) continue;                 /* channel not recorded */
+            const double *e = pos + 3 * el;
             double rho = hypot(e[0] - o[0], e[1] - o[1]);
             if (!((2.0 * p->f_number) * rho <= k * dr)) continue;
             n++;

@@ -65,6 +65,7 @@ class Config(C.Structure):
         ("num_bands", C.c_int32),
         ("band_center_hz", C.c_double * MAX_BANDS), ("band_bandwidth_hz", C.c_double * MAX_BANDS),
         ("band_weight", C.c_double * MAX_BANDS),
+        ("num_channels", C.c_int32), ("channel_element", C.POINTER(C.c_int32)),
     ]
 
 
@@ -146,9 +147,14 @@ def make_config(w, device: int = 0, max_frames: int = 1, **over) -> tuple:
     c.num_bands = len(bands)
     for b, (fc, bw, wt) in enumerate(bands):
         c.band_center_hz[b], c.band_bandwidth_hz[b], c.band_weight[b] = fc, bw, wt
+    chmap = getattr(w, "channel_element", None)
+    if chmap is not None:
+        chmap = np.ascontiguousarray(chmap, np.int32)
+        c.num_channels = chmap.shape[1]
+        c.channel_element = chmap.ctypes.data_as(C.POINTER(C.c_int32))
     for k, v in over.items():
         setattr(c, k, v)
-    return c, (org, dirs, ev)
+    return c, (org, dirs, ev, chmap)
 
 
 def _ptr(t) -> Optional[int]:

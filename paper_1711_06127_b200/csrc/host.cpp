@@ -241,6 +241,22 @@ supra_status validate(const supra_bf_config* c) {
           return fail(SUPRA_E_PARAM, "line_direction[%d] off the uniform angle grid (reading #13/#14)", l);
     }
   }
+  // receive channel map
+  if (c->num_channels < 0) return fail(SUPRA_E_PARAM, "num_channels must be >= 0");
+  if (c->num_channels > 0) {
+    if (!c->channel_element) return fail(SUPRA_E_STRUCT, "channel_element must not be NULL when num_channels > 0");
+    const int nel = c->elements_x * c->elements_y;
+    std::vector<int> seen(nel, -1);
+    for (int e = 0; e < c->num_events; e++)
+      for (int ch = 0; ch < c->num_channels; ch++) {
+        const int el = c->channel_element[(size_t)e * c->num_channels + ch];
+        if (el < -1 || el >= nel) return fail(SUPRA_E_STRUCT, "channel_element[%d][%d] = %d out of range", e, ch, el);
+        if (el >= 0) {
+          if (seen[el] == e) return fail(SUPRA_E_STRUCT, "element %d recorded twice in event %d", el, e);
+          seen[el] = e;
+        }
+      }
+  }
   return SUPRA_OK;
 }
 
@@ -249,16 +265,24 @@ supra_status build_das_tables(supra_bf* h) {
   const supra_bf_config& c = h->cfg;
   const int L = h->L, C = h->C, S = h->S;
   const double dr = h->dr_mm, sc = h->s_per_mm, F = c.f_number;
-  // line groups: lines with bitwise-identical origins share an aperture table
+  // line groups: lines with bitwise-identical origins (and, with a channel
+  // map, events that recorded the same channel -> element map) share an
+  // aperture table
   std::map<std::vector<double>, int> gid;
   std::vector<int32_t> line_group(L);
   std::vector<const double*> g_origin;
+  std::vector<int> g_event;  // an event of the group (its channel map row)
   for (int l = 0; l < L; l++) {
     std::vector<double> key(c.line_origin_mm + 3 * l, c.line_origin_mm + 3 * l + 3);
+    if (c.num_channels > 0) {
+      const int32_t* row = c.channel_element + (size_t)c.line_event[l] * c.num_channels;
+      key.insert(key.end(), row, row + c.num_channels);
+    }
     auto it = gid.find(key);
     if (it == gid.end()) {
       it = gid.emplace(key, (int)g_origin.size()).first;
       g_origin.push_back(c.line_origin_mm + 3 * l);
+      g_event.push_back(c.line_event[l]);
     }
     line_group[l] = it->second;
   }
@@ -270,8 +294,10 @@ supra_status build_das_tables(supra_bf* h) {
     const double* o = g_origin[g];
     auto& v = groups[g];
     for (int ch = 0; ch < C; ch++) {
+      const int el = c.num_channels > 0 ? c.channel_element[(size_t)g_event[g] * c.num_channels + ch] : ch;
+      if (el < 0) continue;  // channel unused in this event
       double e[3];
-      elem_pos(c, ch, e);
+      elem_pos(c, el, e);
       double rho = std::hypot(e[0] - o[0], e[1] - o[1]);
       int ke = k_enter(F, rho, dr, S);
       if (ke >= S) continue;  // never in the aperture within the record
@@ -371,8 +397,9 @@ supra_status build_das_tables(supra_bf* h) {
     const double* d = c.line_direction + 3 * l;
     for (auto& de : groups[line_group[l]]) {
       taps += S - de.kenter;
-      double e3[3];
-      elem_pos(c, de.elem, e3);
+      double e3[3];  // de.elem is the channel; its element from the map
+      elem_pos(c, c.num_channels > 0 ? c.channel_element[(size_t)c.line_event[l] * c.num_channels + de.elem] : de.elem,
+               e3);
       long a = (long)std::floor(tau_d(o, d, e3, de.kenter, dr, fs, c.speed_of_sound_mps, c.t0_s));
       long b = (long)std::floor(tau_d(o, d, e3, S - 1, dr, fs, c.speed_of_sound_mps, c.t0_s)) + 1;
       a = std::max(a, 0L);
@@ -620,7 +647,7 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   supra_bf* h = new supra_bf();
   h->cfg = *cfg;  // the line arrays are read by the builders below, then dropped
   h->L = cfg->num_lines_x * cfg->num_lines_y;
-  h->C = cfg->elements_x * cfg->elements_y;
+  h->C = cfg->num_channels > 0 ? cfg->num_channels : cfg->elements_x * cfg->elements_y;
   h->S = cfg->samples_per_channel;
   h->E = cfg->num_events;
   h->dr_mm = 1000.0 * cfg->speed_of_sound_mps / (2.0 * cfg->sample_frequency_hz);

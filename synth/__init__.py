@@ -42,7 +42,7 @@ class _SynP(C.Structure):
     _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("pitch_x_mm", C.c_double),
                 ("pitch_y_mm", C.c_double), ("E", C.c_int), ("S", C.c_int),
                 ("fs_hz", C.c_double), ("c_mps", C.c_double), ("f0_hz", C.c_double),
-                ("fbw", C.c_double)]
+                ("fbw", C.c_double), ("nch", C.c_int), ("chmap", C.POINTER(C.c_int32))]
 
 
 _cpu = None
@@ -72,7 +72,7 @@ def _gpu_lib():
         L.syn_gpu_frame.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                     C.c_double, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                     C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_ulonglong,
-                                    C.c_double, C.c_void_p]
+                                    C.c_double, C.c_void_p, C.c_int, C.c_void_p]
         L.syn_gpu_frame.restype = C.c_int
         _gpu = L
     return _gpu
@@ -84,8 +84,10 @@ def noise_rel(w: Workload) -> float:
 
 def signal_cpu(w: Workload, scat: np.ndarray, nthreads=None) -> np.ndarray:
     """Noiseless float64 signal [E][C][S] (CPU forward model)."""
+    chm = None if w.channel_element is None else np.ascontiguousarray(w.channel_element, np.int32)
     p = _SynP(w.elements_x, w.elements_y, w.pitch_x_mm, w.pitch_y_mm, w.num_events, w.S, w.fs_hz,
-              w.c_mps, w.center_frequency_hz, w.pulse_fbw)
+              w.c_mps, w.center_frequency_hz, w.pulse_fbw, 0 if chm is None else chm.shape[1],
+              None if chm is None else chm.ctypes.data_as(C.POINTER(C.c_int32)))
     scat = np.ascontiguousarray(scat, np.float64)
     tx = np.ascontiguousarray(w.tx_origin_mm, np.float64)
     out = np.zeros((w.num_events, w.C, w.S), np.float64)
@@ -118,6 +120,9 @@ def channel_data_gpu(w: Workload, out, realisation: int = 0, scat=None):
     sc = torch.as_tensor(np.ascontiguousarray(scat, np.float32), device=dev)
     tx = torch.as_tensor(np.ascontiguousarray(w.tx_origin_mm, np.float32), device=dev)
     scratch = torch.zeros(4, dtype=torch.int32, device=dev)
+    chm = None
+    if w.channel_element is not None:
+        chm = torch.as_tensor(np.ascontiguousarray(w.channel_element, np.int32), device=dev)
     assert out.is_contiguous() and out.dtype == torch.int16
     assert tuple(out.shape) == (w.num_events, w.C, w.S)
     st = torch.cuda.current_stream(dev).cuda_stream
@@ -125,7 +130,9 @@ def channel_data_gpu(w: Workload, out, realisation: int = 0, scat=None):
                                   w.num_events, w.S, w.fs_hz, w.c_mps, w.center_frequency_hz,
                                   w.pulse_fbw, sc.data_ptr(), len(scat), tx.data_ptr(),
                                   out.data_ptr(), scratch.data_ptr(),
-                                  100 + w.seed + realisation, noise_rel(w), st)
+                                  100 + w.seed + realisation, noise_rel(w), st,
+                                  0 if chm is None else chm.shape[1],
+                                  0 if chm is None else chm.data_ptr())
     if rc != 0:
         raise RuntimeError(f"syn_gpu_frame failed: cuda error {rc}")
     torch.cuda.current_stream(dev).synchronize()

@@ -67,6 +67,9 @@ class Workload:
     # frequency compounding: ((center Hz, bandwidth Hz,
     # weight), ...); empty = the single (demod_frequency, demod_bandwidth) band
     bands: tuple = ()
+    # receive channel map [E][channels] -> element (-1 unused); None = one
+    # channel per element ("only 64 channels usable")
+    channel_element: Optional[np.ndarray] = None
     dynamic_range_db: float = 50.0
     reference_mode: int = REF_FRAME_MAX
     reference_value: float = 1.0
@@ -94,6 +97,9 @@ class Workload:
 
     @property
     def C(self) -> int:
+        """Traces per event in the raw frame."""
+        if self.channel_element is not None:
+            return int(np.shape(self.channel_element)[1])
         return self.elements_x * self.elements_y
 
     @property
@@ -210,8 +216,47 @@ def c4(variant: str = "b", **kw) -> Workload:
     return w.replace(**kw) if kw else w
 
 
+def walking_aperture(n_elements: int, n_channels: int, pitch_mm: float,
+                     tx_x_mm: np.ndarray) -> np.ndarray:
+    """Receive channel map of a walking (sliding) active aperture (the
+    128-element probe with 64 usable channels; S:102 leaves the policy open,
+    reading #31): event e records the n_channels contiguous elements whose
+    centre is nearest its transmit position, clamped to the array;
+    channel ch -> element a0(e) + ch.  [E][n_channels] int32."""
+    x0 = -(n_elements - 1) / 2.0 * pitch_mm
+    a0 = np.rint((np.asarray(tx_x_mm) - x0) / pitch_mm - (n_channels - 1) / 2.0).astype(np.int64)
+    a0 = np.clip(a0, 0, n_elements - n_channels)
+    return (a0[:, None] + np.arange(n_channels)[None, :]).astype(np.int32)
+
+
+def table1(tx_events: int = 128, multiline: int = 2, frames: int = 1, **kw) -> Workload:
+    """The paper's 2D benchmark shapes, Table 1 "(a / b)" = (transmit events /
+    multi-line factor): CPLA12875 linear probe, 128 elements,
+    0.3 mm pitch, 7 MHz, 64 usable receive channels (walking aperture), depth
+    45 mm (S = 2368 samples = 45.6 mm at 40 MHz, a multiple of 32),
+    interleaved multi-line: tx_events * M - (M - 1) lines, line l ->
+    event floor(l / M), origins evenly spaced over the element span
+    (S:53); scan conversion on the paper's 0.0225 mm grid."""
+    E, M = tx_events, multiline
+    ev = interleaved_line_events(E, M)
+    L = len(ev)
+    xs = -19.05 + np.arange(L) * (38.1 / (L - 1))
+    o, d = linear_lines(xs)
+    tx = tx_origins(o, ev, E)
+    chm = walking_aperture(128, 64, 0.3, tx[:, 0])
+    s = 0.0225
+    S = 2368
+    nz = int(math.floor(45.0 / s)) + 1                   # 0 .. 45 mm
+    w = Workload(f"T1_{E}_{M}", 128, 1, 0.3, 0.3, 7e6, E, S, L, 1, o, d, ev, tx,
+                 SC_LINEAR_2D, (1694, 1, nz), (-19.05, 0.0, 0.0), (s, s, s), frames=frames,
+                 realisations=min(4, max(1, frames)), noise_db=-60.0, channel_element=chm)
+    return w.replace(**kw) if kw else w
+
+
 CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4a": lambda **k: c4("a", **k),
-           "C4b": lambda **k: c4("b", **k), "C2b": lambda **k: c2("b", **k)}
+           "C4b": lambda **k: c4("b", **k), "C2b": lambda **k: c2("b", **k),
+           "T1_64_1": lambda **k: table1(64, 1, **k), "T1_64_2": lambda **k: table1(64, 2, **k),
+           "T1_128_1": lambda **k: table1(128, 1, **k), "T1_128_2": lambda **k: table1(128, 2, **k)}
 
 
 # ------------------------------------------------------------- scatterers
@@ -221,6 +266,15 @@ def scatterers(w: Workload, realisation: int = 0) -> np.ndarray:
     if name == "C1":
         return np.array([[0.15, 0.0, 600 * dr_mm(w.c_mps, w.fs_hz), 1.0]])
     rng = np.random.Generator(np.random.PCG64(w.seed + realisation))
+    if name.startswith("T1_"):
+        # Table-1 phantom: speckle over the 38.1 x 45 mm field + 3 wires
+        n = 20000
+        x = rng.uniform(-19.05, 19.05, n)
+        z = rng.uniform(1.0, 44.0, n)
+        s = np.zeros((n + 3, 4))
+        s[:n, 0], s[:n, 2], s[:n, 3] = x, z, rng.standard_normal(n)
+        s[n:] = [[-8, 0, 12, 20], [0, 0, 25, 20], [8, 0, 38, 20]]
+        return s
     if name.startswith("C2"):
         n = 20000
         pts = []

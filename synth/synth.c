@@ -29,6 +29,8 @@ typedef struct {
     double pitch_x_mm, pitch_y_mm;
     int E, S;
     double fs_hz, c_mps, f0_hz, fbw;
+    int nch;                 /* 0: channel = element; else traces per event */
+    const int32_t *chmap;    /* [E][nch] element of each channel, -1 = unused (zero trace) */
 } syn_params;
 
 double syn_sigma_samples(double fs_hz, double f0_hz, double fbw)
@@ -50,18 +52,20 @@ static void *syn_worker(void *arg)
 {
     syn_job *j = (syn_job *)arg;
     const syn_params *p = j->p;
-    const int C = p->nx * p->ny, S = p->S;
+    const int C = p->nch > 0 ? p->nch : p->nx * p->ny, S = p->S;
     const double sig = syn_sigma_samples(p->fs_hz, p->f0_hz, p->fbw);
     const double half = 4.0 * sig;
     const double w0 = 2.0 * M_PI * p->f0_hz / p->fs_hz;
     const double smm = p->fs_hz / (1000.0 * p->c_mps);
     for (long tr = j->t; tr < (long)p->E * C; tr += j->nt) {
         int ev = (int)(tr / C), ch = (int)(tr % C);
-        int i = ch % p->nx, jj = ch / p->nx;
+        int el = p->nch > 0 ? p->chmap[(size_t)ev * p->nch + ch] : ch;
+        int i = el % p->nx, jj = el / p->nx;
         double ex = (i - (p->nx - 1) / 2.0) * p->pitch_x_mm;
         double ey = (jj - (p->ny - 1) / 2.0) * p->pitch_y_mm;
         double *o = j->out + (size_t)tr * S;
         for (int n = 0; n < S; n++) o[n] = 0.0;
+        if (el < 0) continue;
         const double *t = j->tx + 3 * ev;
         for (int s = 0; s < j->nscat; s++) {
             const double *q = j->scat + 4 * s;

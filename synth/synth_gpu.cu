@@ -23,7 +23,14 @@ struct SynP {
   float smm;     // fs / (1000 c): samples per mm of path
   float sigma;   // pulse sigma in samples
   float w0;      // 2 pi f0 / fs
+  int nch;                 // 0: channel = element; else traces per event
+  const int32_t* chmap;    // [E][nch] element of each channel, -1 = unused (zero trace)
 };
+
+__device__ __forceinline__ int channels(const SynP& p) { return p.nch > 0 ? p.nch : p.nx * p.ny; }
+__device__ __forceinline__ int channel_elem(const SynP& p, int ev, int ch) {
+  return p.nch > 0 ? p.chmap[(size_t)ev * p.nch + ch] : ch;
+}
 
 __device__ __forceinline__ void elem_pos(const SynP& p, int ch, float& ex, float& ey) {
   int i = ch % p.nx, j = ch / p.nx;
@@ -33,14 +40,15 @@ __device__ __forceinline__ void elem_pos(const SynP& p, int ch, float& ex, float
 
 __global__ void k_bound(SynP p, const float4* __restrict__ scat, int n,
                         const float* __restrict__ tx, unsigned* __restrict__ bound_bits) {
-  const int C = p.nx * p.ny;
+  const int C = channels(p);
   const int tr = blockIdx.x;
   const int ev = tr / C, ch = tr % C;
+  const int el = channel_elem(p, ev, ch);
   float ex, ey;
-  elem_pos(p, ch, ex, ey);
+  elem_pos(p, el, ex, ey);
   const float tx0 = tx[3 * ev], tx1 = tx[3 * ev + 1], tx2 = tx[3 * ev + 2];
   float acc = 0.f;
-  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+  for (int s = threadIdx.x; s < (el < 0 ? 0 : n); s += blockDim.x) {
     float4 q = scat[s];
     float dtx = sqrtf((q.x - tx0) * (q.x - tx0) + (q.y - tx1) * (q.y - tx1) + (q.z - tx2) * (q.z - tx2));
     float drx = sqrtf((q.x - ex) * (q.x - ex) + (q.y - ey) * (q.y - ey) + q.z * q.z);
@@ -77,20 +85,21 @@ __global__ void k_trace(SynP p, const float4* __restrict__ scat, int n, const fl
                         const unsigned* __restrict__ bound_bits, int* __restrict__ peak_fixed,
                         int16_t* __restrict__ out, unsigned long long seed, float noise_rel) {
   extern __shared__ int trace[];
-  const int C = p.nx * p.ny;
+  const int C = channels(p);
   const int tr = blockIdx.x;
   const int ev = tr / C, ch = tr % C;
+  const int el = channel_elem(p, ev, ch);
   const int S = p.S;
   for (int i = threadIdx.x; i < S; i += blockDim.x) trace[i] = 0;
   __syncthreads();
   const float B = __uint_as_float(*bound_bits);
   const float fx = (B > 0.f) ? 1073741824.f / B : 0.f;
   float ex, ey;
-  elem_pos(p, ch, ex, ey);
+  elem_pos(p, el, ex, ey);
   const float tx0 = tx[3 * ev], tx1 = tx[3 * ev + 1], tx2 = tx[3 * ev + 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const float half = 4.f * p.sigma, inv2s2 = 1.f / (2.f * p.sigma * p.sigma);
-  for (int s = warp; s < n; s += nw) {
+  for (int s = warp; s < (el < 0 ? 0 : n); s += nw) {
     float4 q = scat[s];
     float dtx = sqrtf((q.x - tx0) * (q.x - tx0) + (q.y - tx1) * (q.y - tx1) + (q.z - tx2) * (q.z - tx2));
     float drx = sqrtf((q.x - ex) * (q.x - ex) + (q.y - ey) * (q.y - ey) + q.z * q.z);
@@ -139,7 +148,7 @@ extern "C" {
 int syn_gpu_frame(int nx, int ny, double px, double py, int E, int S, double fs_hz, double c_mps,
                   double f0_hz, double fbw, const void* scat_dev, int n, const void* tx_dev,
                   void* out_dev, void* scratch_dev, unsigned long long seed, double noise_rel,
-                  void* stream) {
+                  void* stream, int nch, const void* chmap_dev) {
   cudaStream_t st = (cudaStream_t)stream;
   SynP p;
   p.nx = nx; p.ny = ny; p.px = (float)px; p.py = (float)py; p.E = E; p.S = S;
@@ -147,10 +156,12 @@ int syn_gpu_frame(int nx, int ny, double px, double py, int E, int S, double fs_
   double sigma_f = fbw * f0_hz / (2.0 * 1.1774100225154747);
   p.sigma = (float)(fs_hz / (6.283185307179586 * sigma_f));
   p.w0 = (float)(6.283185307179586 * f0_hz / fs_hz);
+  p.nch = nch;
+  p.chmap = (const int32_t*)chmap_dev;
   unsigned* bound = (unsigned*)scratch_dev;
   int* peak = (int*)scratch_dev + 1;
   cudaMemsetAsync(scratch_dev, 0, 8, st);
-  const int traces = E * nx * ny;
+  const int traces = E * (nch > 0 ? nch : nx * ny);
   if (traces == 0) return 0;
   k_bound<<<traces, 256, 0, st>>>(p, (const float4*)scat_dev, n, (const float*)tx_dev, bound);
   size_t sm = (size_t)S * sizeof(int);

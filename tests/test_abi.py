@@ -141,3 +141,13 @@ def test_band_bank_errors(bands):
         return
     rc, msg = _create(w)
     assert rc == binding.E_PARAM and "band" in msg, (rc, msg)
+
+
+def test_channel_map_errors():
+    w = configs.table1(64, 1)
+    bad = w.channel_element.copy()
+    bad[5, 3] = bad[5, 4]                            # element twice in one event
+    assert _create(w.replace(channel_element=bad))[0] == binding.E_STRUCT
+    bad = w.channel_element.copy()
+    bad[0, 0] = 128                                  # not an element
+    assert _create(w.replace(channel_element=bad))[0] == binding.E_STRUCT

@@ -211,9 +211,16 @@ def _brute_force_das(w, raw):
     pos = np.concatenate([pos, np.zeros((len(pos), 1))], 1)
     dr = w.c_mps * 1e3 / (2 * w.fs_hz)
     out = np.zeros((w.L, w.S))
+    allpos = pos
     for l in range(w.L):
         o, d = w.line_origin_mm[l], w.line_direction[l]
         x = raw[w.line_event[l]].astype(np.float64)
+        if w.channel_element is not None:      # receive channel map
+            els = np.asarray(w.channel_element[w.line_event[l]])
+            x = x[els >= 0]
+            pos = allpos[els[els >= 0]]
+        else:
+            pos = allpos
         xp = np.concatenate([x, np.zeros((x.shape[0], 2))], 1)
         rho = np.hypot(pos[:, 0] - o[0], pos[:, 1] - o[1])
         for k in range(w.S):
@@ -267,3 +274,65 @@ def test_determinism_threads():
     a = oracle.das(w, raw, nthreads=1)
     b = oracle.das(w, raw, nthreads=7)
     assert np.array_equal(a, b)
+
+
+# --------------------------------------- receive channel map (Table 1, f2)
+# P:161 "only 64 channels usable" for the 128-element probe; S:102 active
+# aperture; S:57/S:147 interleaved multi-line; P:337 Table-1 shapes.
+
+@pytest.mark.parametrize("E,M,L", [(64, 1, 64), (64, 2, 127), (128, 1, 128), (128, 2, 255)])
+def test_table1_shapes_P337(E, M, L):
+    w = configs.table1(E, M)
+    assert w.L == L and w.num_events == E and w.C == 64 and w.S * configs.dr_mm() >= 45.0
+    assert w.line_event[-1] == E - 1
+    if M == 2:
+        assert w.line_event[L - 1] == E - 1 and w.line_event[3] == 1
+    # every event records 64 contiguous elements holding its transmit position
+    ex = configs.element_x(128, 0.3)
+    for e in range(E):
+        els = w.channel_element[e]
+        assert np.array_equal(els, np.arange(els[0], els[0] + 64))
+        assert ex[els[0]] - 0.15 <= w.tx_origin_mm[e, 0] <= ex[els[-1]] + 0.15
+
+
+def test_identity_channel_map_equals_no_map():
+    w = tiny_linear(n_el=16, S=256)
+    rng = np.random.default_rng(8)
+    raw = rng.integers(-3000, 3000, (w.num_events, w.C, w.S)).astype(np.int16)
+    ident = np.tile(np.arange(16, dtype=np.int32), (w.num_events, 1))
+    assert np.array_equal(oracle.das(w, raw), oracle.das(w.replace(channel_element=ident), raw))
+
+
+def test_walking_aperture_constant_input_counts_recorded_members():
+    # rect window, normalize none, x == 1: RF = number of RECORDED aperture
+    # members wherever every member's tau <= S - 1 (the north-star pin,
+    # restricted to the event's active channels)
+    w0 = tiny_linear(n_el=32, S=512, window=configs.WIN_RECT, normalize=configs.NORM_NONE)
+    chm = configs.walking_aperture(32, 8, 0.3, w0.tx_origin_mm[:, 0])
+    w = w0.replace(channel_element=chm)
+    raw = np.ones((w.num_events, 8, w.S), np.int16)
+    rf = oracle.das(w, raw)
+    ex = configs.element_x(32, 0.3)
+    dr = configs.dr_mm()
+    for l in (0, 9, 31):
+        rec = ex[chm[w.line_event[l]]]
+        for k in (40, 120, 200):
+            n = int(np.sum(2.0 * w.f_number * np.abs(rec - w.line_origin_mm[l, 0]) <= k * dr))
+            assert rf[l, k] == n
+
+
+def test_bruteforce_walking_aperture_multiline_S570():
+    w0 = tiny_linear(n_el=24, S=256)
+    E, M = 12, 2
+    ev = configs.interleaved_line_events(E, M)
+    L = len(ev)
+    o, d = configs.linear_lines(-(23 / 2) * 0.3 + np.arange(L) * (23 * 0.3 / (L - 1)))
+    tx = configs.tx_origins(o, ev, E)
+    chm = configs.walking_aperture(24, 10, 0.3, tx[:, 0])
+    chm[3, 4] = -1                                   # an unused channel
+    w = w0.replace(num_events=E, num_lines_x=L, line_origin_mm=o, line_direction=d, line_event=ev,
+                   tx_origin_mm=tx, channel_element=chm)
+    raw = np.random.default_rng(9).integers(-3000, 3000, (E, 10, w.S)).astype(np.int16)
+    a = oracle.das(w, raw)
+    b = _brute_force_das(w, raw)
+    assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))

@@ -351,3 +351,29 @@ def test_c2_frequency_compounding_batch():
         e_rf, e_db, _, _ = check_frame(w, raw[f].cpu().numpy(), rf_g[f], y_g[f])
         assert e_rf <= RF_TOL, (f, e_rf)
         assert e_db <= DB_TOL, (f, e_db)
+
+
+# ---------------------------------- Table-1 acquisition shapes (f2)
+@pytest.mark.parametrize("E,M", [(64, 1), (128, 2)])
+def test_table1_shape_full_chain(E, M):
+    w = configs.table1(E, M)
+    raw = raw_frames(w, 1)
+    bf = SupraBF(w)
+    rf_g, y_g = run_gpu(bf, raw, 1)
+    e_rf, e_db, _, _ = check_frame(w, raw[0].cpu().numpy(), rf_g[0], y_g[0])
+    assert e_rf <= RF_TOL, e_rf
+    assert e_db <= DB_TOL, e_db
+
+
+def test_table1_batch_and_scan_conversion():
+    w = configs.table1(64, 2, sc_output_type=configs.T_U8)
+    F = 3
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    rf_g, y_g = run_gpu(bf, raw, F)
+    e_rf, e_db, _, _ = check_frame(w, raw[2].cpu().numpy(), rf_g[2], y_g[2])
+    assert e_rf <= RF_TOL and e_db <= DB_TOL, (e_rf, e_db)
+    valid_o, idx_o, _ = oracle.sc_table(w)
+    valid_g, idx_g = bf.sc_indices()
+    assert np.array_equal(valid_g, valid_o)
+    assert np.array_equal(idx_g[valid_o.astype(bool)], idx_o[valid_o.astype(bool)])
