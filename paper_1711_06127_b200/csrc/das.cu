@@ -43,7 +43,7 @@ struct SmemLayout {
   int16_t* stage;   // [NS][stage_bytes]
   float4* line;     // FIR line buffer, aliases the stage ring between passes
   float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
-  int2* wse;        // [nent] {window start ws, channel}
+  int2* wse;        // [nent] {window start ws, channel | rcut << 20}
   float4* carry;    // [ngroups][2P] RF tail of the previous pass
   uint64_t* full;   // [kMaxStages]
   unsigned* rel;    // [kMaxStages] warps done with the slot (last one refills it)
@@ -288,6 +288,9 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
+  if (a.raw_maps && (int)threadIdx.x < S / kRowSamples)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.raw_maps + threadIdx.x))
+                 : "memory");
   if (threadIdx.x < 16) sm.smax[threadIdx.x] = 0u;
 
   const int kt = threadIdx.x;
@@ -326,16 +329,26 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       const float hb = 0.5f * (float)kb;
       const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
       const int ws = ((int)floorf(tb) - 2) & ~(kRowSamples - 1);
+      // exclusive end row of the pass's referenced samples: i0 + 1 <=
+      // floor(tau(kend - 1)) + 1 for every member k < kend (+1 margin)
+      const int kl = kend - 1;
+      const float hl = 0.5f * (float)kl;
+      const float tl = (float)kl + split_delay(Ah, B, hl, kl > 0 ? hl * hl : 1e-20f) + a.t0fs;
+      const int rcut = max(1, min(S / kRowSamples, ((int)floorf(tl) + 3 + kRowSamples - 1) / kRowSamples));
       sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(e.kenter));
-      sm.wse[i] = make_int2(ws, e.elem);
+      sm.wse[i] = make_int2(ws, e.elem | (rcut << 20));
     }
     __syncthreads();  // records visible; the previous pass is done with the line buffer
 
     // TMA of entry jj's window (all FB frames) into ring slot `buf`.
     auto produce = [&](int jj, int buf) {
       const int2 we = sm.wse[jj];
+      // rows at or past rcut are out of bounds in raw_maps[rcut - 1]: zero
+      // fill, no DRAM read (the box size, and so the tx count, is fixed)
+      const CUtensorMap* m = a.raw_maps ? a.raw_maps + ((we.y >> 20) - 1) : &tmap;
       mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
-      tma_load_5d((unsigned char*)sm.stage + buf * SB, &tmap, 0, we.x / kRowSamples, we.y, ev, fm, &sm.full[buf]);
+      tma_load_5d((unsigned char*)sm.stage + buf * SB, m, 0, we.x / kRowSamples, we.y & 0xFFFFF, ev, fm,
+                  &sm.full[buf]);
     };
     if (threadIdx.x == 0 && a.debug_skip != 2) {
       // the ring was last written through the generic proxy (line buffer)

@@ -88,6 +88,16 @@ struct supra_bf {
   float band_w[kMaxBands] = {1.f, 0.f, 0.f, 0.f};
   std::vector<float> fir_c, fir_s;  // [kMaxBands][kMaxHalfTaps + 1]
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
+  // per-(raw buffer, frames, shape) sets of row-cut tensor maps (DasArgs::
+  // raw_maps), encoded once and kept on the device; small LRU
+  struct MapSet {
+    const void* raw = nullptr;
+    int F = 0, fb = 0, nt = 0;
+    CUtensorMap* d = nullptr;  // device [S/32]
+    CUtensorMap* h = nullptr;  // pinned host staging
+  };
+  MapSet mcache[4];
+  int mnext = 0;
   int64_t info[8] = {0};
 };
 
@@ -107,6 +117,11 @@ void free_all(supra_bf* h) {
                   h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_blk_kmin, h->d_col_l0, h->d_col_nl, h->d_rows, h->d_ent};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& m : h->mcache) {
+    if (m.d) cudaFree(m.d);
+    if (m.h) cudaFreeHost(m.h);
+    m = supra_bf::MapSet{};
+  }
 }
 
 // Element (i,j) position, S:30 (same definition the oracle writes out).
@@ -588,10 +603,13 @@ EncodeTiledFn encode_fn() {
 // dims {16, S/32, C, E, F}; box {16, rows, 1, 1, fb} -- one TMA per
 // (aperture entry, depth pass, frame group) fetches the pass's trace window;
 // out-of-bounds rows (before 0 or past S) and frames (>= F) read as zero.
-bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, int rows, int fb) {
+// rows_in_range < S/32 cuts the time extent (rows past it read as zeros).
+bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, int rows, int fb,
+                  int rows_in_range = -1) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[5] = {16, (cuuint64_t)S / kRowSamples, (cuuint64_t)C, (cuuint64_t)E, (cuuint64_t)F};
+  const cuuint64_t R = rows_in_range > 0 ? (cuuint64_t)rows_in_range : (cuuint64_t)S / kRowSamples;
+  cuuint64_t dims[5] = {16, R, (cuuint64_t)C, (cuuint64_t)E, (cuuint64_t)F};
   cuuint64_t strides[4] = {(cuuint64_t)kRowSamples * 2, (cuuint64_t)S * 2, (cuuint64_t)C * S * 2,
                            (cuuint64_t)E * C * S * 2};
   cuuint32_t box[5] = {16, (cuuint32_t)rows, 1, 1, (cuuint32_t)fb};
@@ -599,6 +617,43 @@ bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, i
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<void*>(raw), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Row-cut map set for DasArgs::raw_maps: m[r-1] = make_raw_map with only r
+// time rows in range.  Cached per (raw, F, fb, nt); NULL on failure (the
+// kernel then uses its single map).
+const CUtensorMap* row_cut_maps(supra_bf* h, const void* raw, int F, int fb, int nt, cudaStream_t st) {
+  for (auto& m : h->mcache)
+    if (m.d && m.raw == raw && m.F == F && m.fb == fb && m.nt == nt) return m.d;
+  const int R = h->S / kRowSamples;
+  auto& m = h->mcache[h->mnext];
+  h->mnext = (h->mnext + 1) % 4;
+  if (!m.d && cudaMalloc((void**)&m.d, sizeof(CUtensorMap) * (kMaxSamples / kRowSamples)) != cudaSuccess) {
+    cudaGetLastError();
+    m.d = nullptr;
+    return nullptr;
+  }
+  if (!m.h && cudaMallocHost((void**)&m.h, sizeof(CUtensorMap) * (kMaxSamples / kRowSamples)) != cudaSuccess) {
+    cudaGetLastError();
+    m.h = nullptr;
+    return nullptr;
+  }
+  // an evicted slot's previous upload may still be pending on the stream
+  if (m.raw) cudaStreamSynchronize(st);
+  m.raw = nullptr;
+  for (int r = 1; r <= R; r++)
+    if (!make_raw_map(&m.h[r - 1], raw, F, h->E, h->C, h->S, das_rows_nt(nt), fb, r)) return nullptr;
+  // ordered before the kernel on the same stream; the staging buffer is not
+  // rewritten while this entry stays cached
+  if (cudaMemcpyAsync(m.d, m.h, sizeof(CUtensorMap) * R, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  m.raw = raw;
+  m.F = F;
+  m.fb = fb;
+  m.nt = nt;
+  return m.d;
 }
 
 bool is_device_ptr(const void* p, int dev) {
@@ -782,6 +837,10 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.Fmap = Fmain;
   a.pdl_trigger = rem > 0;
   a.pdl_wait_end = 0;
+  // exact trace windows for the multi-pass / multi-frame kernel (the
+  // single-frame kernel's windows run to the end of the record anyway)
+  const bool exact = !std::getenv("SUPRA_BF_NO_ROWCUT");
+  a.raw_maps = (exact && !das_warp_ok(sh.fb, h->S, a.t0fs)) ? row_cut_maps(h, raw, Fmain, sh.fb, sh.nt, st) : nullptr;
   if (h->ev_before) cudaEventRecord(h->ev_before, st);
   supra_status s = check_launch(launch_das(tm, a, sh, st), "das kernel");
   if (s == SUPRA_OK && rem) {
@@ -790,6 +849,9 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
     a2.Fmap = rem;
     a2.pdl_trigger = 0;
     a2.pdl_wait_end = 1;
+    a2.raw_maps = (exact && !das_warp_ok(sh2.fb, h->S, a.t0fs))
+                      ? row_cut_maps(h, (const char*)raw + Fmain * frame_bytes, rem, sh2.fb, sh2.nt, st)
+                      : nullptr;
     s = check_launch(launch_das(tm2, a2, sh2, st), "das kernel (remainder frames)");
   }
   if (h->ev_after) cudaEventRecord(h->ev_after, st);

@@ -85,6 +85,12 @@ struct DasArgs {
   int y_type;                  // SUPRA_T_F32 / SUPRA_T_U8
   unsigned* frame_max;         // [F] float bits (frame-max mode)
   int debug_skip;              // measurement only: skip the tap loop (TMA pipeline alone)
+  // [S/32] tensor maps in global memory identical to the launch's map except
+  // for the time extent: raw_maps[r - 1] has r rows in range, so a window box
+  // whose rows past the pass's last referenced row are out of bounds reads
+  // them as zeros without DRAM traffic (exact windows, one TMA per entry).
+  // NULL: every window uses the launch's map.
+  const CUtensorMap* raw_maps;
 };
 
 struct EnvArgs {  // standalone epilogue on an RF buffer
