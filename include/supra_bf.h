@@ -54,6 +54,7 @@ typedef enum {
 } supra_status;
 
 enum { SUPRA_WIN_RECT = 0, SUPRA_WIN_HANN = 1, SUPRA_WIN_HAMMING = 2 }; /* receive window */
+enum { SUPRA_INTERP_LINEAR = 0, SUPRA_INTERP_NEAREST = 1 };           /* fractional-delay lookup */
 enum { SUPRA_NORM_COUNT = 0, SUPRA_NORM_NONE = 1 };   /* sum / #members (reading #7) or plain sum */
 enum { SUPRA_REF_FRAME_MAX = 0, SUPRA_REF_FIXED = 1 };/* log reference */
 enum { SUPRA_T_I16 = 0, SUPRA_T_F32 = 1, SUPRA_T_U8 = 2 };
@@ -140,6 +141,10 @@ typedef struct {
      * SUPRA_E_STRUCT. */
     int32_t num_channels;
     const int32_t *channel_element;
+    /* fractional-delay sample lookup ("interpolation: {nearest,
+     * linear}"): LINEAR (default) x~(tau) = (1-f) x~[i0] + f x~[i0+1];
+     * NEAREST x~(tau) = x~[floor(tau + 1/2)] (reading #32). */
+    int32_t interpolation;
 } supra_bf_config;
 
 /*

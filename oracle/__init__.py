@@ -44,7 +44,7 @@ class _DasParams(C.Structure):
                 ("origin_mm", C.POINTER(C.c_double)), ("direction", C.POINTER(C.c_double)),
                 ("line_event", C.POINTER(C.c_int32)),
                 ("f_number", C.c_double), ("window", C.c_int), ("normalize", C.c_int),
-                ("nch", C.c_int), ("chmap", C.POINTER(C.c_int32))]
+                ("nch", C.c_int), ("chmap", C.POINTER(C.c_int32)), ("interp", C.c_int)]
 
 
 class _ScParams(C.Structure):
@@ -130,7 +130,8 @@ def das(cfg, raw, lines=None, nthreads=None):
                    cfg.fs_hz, cfg.c_mps, cfg.t0_s, L, _dptr(org), _dptr(dirs),
                    ev.ctypes.data_as(C.POINTER(C.c_int32)), cfg.f_number, cfg.window,
                    cfg.normalize, nch,
-                   None if chmap is None else chmap.ctypes.data_as(C.POINTER(C.c_int32)))
+                   None if chmap is None else chmap.ctypes.data_as(C.POINTER(C.c_int32)),
+                   int(getattr(cfg, "interpolation", 0)))
     rf = np.zeros((len(lines), S), np.float64)
     nt = nthreads or min(len(lines), os.cpu_count() or 1)
     rc = lib().ora_das(C.byref(p), raw.ctypes.data, lines.ctypes.data, len(lines), _dptr(rf),

@@ -99,6 +99,9 @@ typedef struct {
      * elements its event recorded.                                       */
     int nch;
     const int32_t *chmap;
+    /* fractional-delay lookup: 0 linear (reading #10), 1 nearest:
+     * x~[floor(tau + 1/2)] (reading #32, ties round up)                  */
+    int interp;
 } ora_das_params;
 
 /* Delay-and-sum with dynamic receive focusing (S:133,
@@ -132,7 +135,8 @@ static void ora_das_line(const ora_das_params *p, const double *pos, const int16
             long i0 = (long)fl;
             double f = tau - fl;
             const int16_t *x = xev + (size_t)ch * (size_t)S;
-            double v = (1.0 - f) * ora_sample(x, i0, S) + f * ora_sample(x, i0 + 1, S);
+            double v = (p->interp == 1) ? ora_sample(x, (long)floor(tau + 0.5), S)
+                                        : (1.0 - f) * ora_sample(x, i0, S) + f * ora_sample(x, i0 + 1, S);
             double R = z / (2.0 * p->f_number);
             double u = (R > 0.0) ? rho / R : 0.0;
             double w = ora_window(p->window, u);

@@ -22,6 +22,7 @@ ABI_VERSION = 2
 MAX_BANDS = 4
 OK, E_PARAM, E_STRUCT, E_RESOURCE, E_CUDA = 0, 2, 3, 4, 5
 WIN_RECT, WIN_HANN, WIN_HAMMING = 0, 1, 2
+INTERP_LINEAR, INTERP_NEAREST = 0, 1
 NORM_COUNT, NORM_NONE = 0, 1
 REF_FRAME_MAX, REF_FIXED = 0, 1
 T_I16, T_F32, T_U8 = 0, 1, 2
@@ -66,6 +67,7 @@ class Config(C.Structure):
         ("band_center_hz", C.c_double * MAX_BANDS), ("band_bandwidth_hz", C.c_double * MAX_BANDS),
         ("band_weight", C.c_double * MAX_BANDS),
         ("num_channels", C.c_int32), ("channel_element", C.POINTER(C.c_int32)),
+        ("interpolation", C.c_int32),
     ]
 
 
@@ -147,6 +149,7 @@ def make_config(w, device: int = 0, max_frames: int = 1, **over) -> tuple:
     c.num_bands = len(bands)
     for b, (fc, bw, wt) in enumerate(bands):
         c.band_center_hz[b], c.band_bandwidth_hz[b], c.band_weight[b] = fc, bw, wt
+    c.interpolation = getattr(w, "interpolation", 0)
     chmap = getattr(w, "channel_element", None)
     if chmap is not None:
         chmap = np.ascontiguousarray(chmap, np.int32)

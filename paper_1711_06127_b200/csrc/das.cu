@@ -171,7 +171,7 @@ __device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4
   if (T0) delta += a.t0fs;
   const float tf = __fadd_rd(delta, kFloorMagic);
   const int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - k0 - kt)
-  const float fr = delta - (tf - kFloorMagic);
+  const float fr = (delta - (tf - kFloorMagic)) * a.fr_scale;
   float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
   w = mem ? w : 0.f;
   // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
@@ -197,7 +197,8 @@ __device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4&
   const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
   const int idx0 = __float_as_int(tf.x) - wsm + m * kTileK;
   const int idx1 = __float_as_int(tf.y) - wsm + (m + 1) * kTileK;
-  const float2 fr = sub2(delta, sub2(tf, make_float2(kFloorMagic, kFloorMagic)));
+  const float2 fr = __fmul2_rn(sub2(delta, sub2(tf, make_float2(kFloorMagic, kFloorMagic))),
+                               make_float2(a.fr_scale, a.fr_scale));
   const float2 u = __fmul2_rn(make_float2(r.z, r.z),
                               make_float2(rcp_ftz(fmaxf(kf.x, 1.f)), rcp_ftz(fmaxf(kf.y, 1.f))));
   float2 w = __ffma2_rn(make_float2(__cosf(u.x), __cosf(u.y)), make_float2(a.win_b, a.win_b),

@@ -87,14 +87,14 @@ __device__ __forceinline__ int entry_ws(const DasEntry& e, const float4& dir, fl
 }
 
 // Tile pair (2p, 2p+1): output samples k = 64 p + lane and k + 32.
-template <int PP, bool HANN, bool T0>
+template <int PP, bool HANN, int MODE>
 __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, const float2* rkt, int lane,
                                          float2 lanef, float2& acc) {
   const float2 h = __ffma2_rn(lanef, make_float2(0.5f, 0.5f), make_float2(32.0f * PP, 32.0f * PP + 16.0f));
   float2 hh = __fmul2_rn(h, h);
   if (PP == 0 && lane == 0) hh.x = 1e-20f;  // r2 > 0 even at k = 0, q = 0
   float2 delta = split_delay2(c.Ah, c.B, h, hh);
-  if (T0) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));
+  if (MODE >= 1) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));  // t0 (+ 1/2 for nearest)
   const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
   const int idx0 = __float_as_int(tf.x) - c.wsl + 64 * PP;
   const int idx1 = __float_as_int(tf.y) - c.wsl + 64 * PP + 32;
@@ -120,9 +120,13 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
   // FP32 ops per pair (the FP32 pipe, not issue, bounds this kernel)
   const uint32_t p0 = c.sbase + 2u * (uint32_t)idx0, p1 = c.sbase + 2u * (uint32_t)idx1;
   const float2 x0 = make_float2(lds_s16f(p0, 0), lds_s16f(p1, 0));
-  const float2 x1 = make_float2(lds_s16f(p0, 2), lds_s16f(p1, 2));
-  const float2 v = __ffma2_rn(fr, sub2(x1, x0), x0);
-  acc = __ffma2_rn(w, v, acc);
+  if constexpr (MODE == 2) {  // nearest sample x~[floor(tau + 1/2)]
+    acc = __ffma2_rn(w, x0, acc);
+  } else {
+    const float2 x1 = make_float2(lds_s16f(p0, 2), lds_s16f(p1, 2));
+    const float2 v = __ffma2_rn(fr, sub2(x1, x0), x0);
+    acc = __ffma2_rn(w, v, acc);
+  }
 }
 
 // Pairs from the group of kGroup pairs holding p0 to NP-1 (NP = NTL / 2),
@@ -132,20 +136,20 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
 // serialises the pairs' dependency chains); the up to kGroup - 1 extra
 // leading pairs carry zero weight (k < k_enter).
 constexpr int kGroup = 4;
-template <int G0, int NP, bool HANN, bool T0>
+template <int G0, int NP, bool HANN, int MODE>
 __device__ __forceinline__ void pair_group(const DasArgs& a, const EntryCtx& c, const float2* rkt, int lane,
                                            float2 lanef, float2* acc) {
   constexpr int q = G0 * kGroup < NP ? G0 * kGroup : 0;
-  pair_tap<q + 0, HANN, T0>(a, c, rkt, lane, lanef, acc[q + 0]);
-  pair_tap<q + 1, HANN, T0>(a, c, rkt, lane, lanef, acc[q + 1]);
-  pair_tap<q + 2, HANN, T0>(a, c, rkt, lane, lanef, acc[q + 2]);
-  pair_tap<q + 3, HANN, T0>(a, c, rkt, lane, lanef, acc[q + 3]);
+  pair_tap<q + 0, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 0]);
+  pair_tap<q + 1, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 1]);
+  pair_tap<q + 2, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 2]);
+  pair_tap<q + 3, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 3]);
 }
 #define SUPRA_GROUP(g)                                                              \
   case g:                                                                          \
-    if constexpr ((g) * kGroup < NP) pair_group<(g), NP, HANN, T0>(a, c, rkt, lane, lanef, acc); \
+    if constexpr ((g) * kGroup < NP) pair_group<(g), NP, HANN, MODE>(a, c, rkt, lane, lanef, acc); \
     [[fallthrough]];
-template <int NP, bool HANN, bool T0>
+template <int NP, bool HANN, int MODE>
 __device__ __forceinline__ void entry_pairs(int p0, const DasArgs& a, const EntryCtx& c, const float2* rkt, int lane,
                                             float2 lanef, float2* acc) {
   static_assert(NP % kGroup == 0 && NP / kGroup <= 8, "pair groups");
@@ -162,7 +166,7 @@ __device__ __forceinline__ void entry_pairs(int p0, const DasArgs& a, const Entr
 
 // NTL = S / 32 tiles per lane (32 or 64); the raw tensor map is das.cu's
 // with box rows das_rows_nt(NTL / 8) (the whole record from a window start).
-template <int NTL, bool HANN, bool T0>
+template <int NTL, bool HANN, int MODE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __grid_constant__ CUtensorMap tmap,
                                                          const DasArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     // (they would be spilled to local memory)
     float2 lf = lanef;
     asm volatile("" : "+f"(lf.x), "+f"(lf.y));
-    if (a.debug_skip != 1) entry_pairs<NP, HANN, T0>(e.kenter >> 6, a, c, rkt, lane, lf, acc);
+    if (a.debug_skip != 1) entry_pairs<NP, HANN, MODE>(e.kenter >> 6, a, c, rkt, lane, lf, acc);
     __syncwarp();
     if (lane == 0 && j + kWarps * NSW < np && a.debug_skip != 2) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -298,10 +302,10 @@ size_t das_warp_smem_bytes(int S, int fir_taps) {
   return warp_layout(S, S / 32 + 2, (fir_taps - 1) / 2).total;
 }
 
-template <int NTL, bool HANN, bool T0>
+template <int NTL, bool HANN, int MODE>
 static cudaError_t launch_w(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
   const size_t smem = das_warp_smem_bytes(NTL * 32, a.fir_taps);
-  auto kern = das_warp_kernel<NTL, HANN, T0>;
+  auto kern = das_warp_kernel<NTL, HANN, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -317,15 +321,17 @@ static cudaError_t launch_w(const CUtensorMap& tm, const DasArgs& a, cudaStream_
   return cudaLaunchKernelEx(&cfg, kern, tm, a);
 }
 
-template <bool HANN, bool T0>
+template <bool HANN, int MODE>
 static cudaError_t launch_w2(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
-  return a.S == 1024 ? launch_w<32, HANN, T0>(tm, a, st) : launch_w<64, HANN, T0>(tm, a, st);
+  return a.S == 1024 ? launch_w<32, HANN, MODE>(tm, a, st) : launch_w<64, HANN, MODE>(tm, a, st);
 }
 
 cudaError_t launch_das_warp(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
   const bool hann = a.win_a == 0.5f && a.win_b == 0.5f;
-  if (a.t0fs != 0.f) return hann ? launch_w2<true, true>(tm, a, st) : launch_w2<false, true>(tm, a, st);
-  return hann ? launch_w2<true, false>(tm, a, st) : launch_w2<false, false>(tm, a, st);
+  const int mode = a.fr_scale == 0.f ? 2 : (a.t0fs != 0.f ? 1 : 0);
+  if (mode == 2) return hann ? launch_w2<true, 2>(tm, a, st) : launch_w2<false, 2>(tm, a, st);
+  if (mode == 1) return hann ? launch_w2<true, 1>(tm, a, st) : launch_w2<false, 1>(tm, a, st);
+  return hann ? launch_w2<true, 0>(tm, a, st) : launch_w2<false, 0>(tm, a, st);
 }
 
 }  // namespace supra

@@ -174,6 +174,8 @@ supra_status validate(const supra_bf_config* c) {
   if (!(c->f_number > 0)) return fail(SUPRA_E_PARAM, "f_number must be > 0 (S:126)");
   if (c->window < SUPRA_WIN_RECT || c->window > SUPRA_WIN_HAMMING) return fail(SUPRA_E_PARAM, "window");
   if (c->normalize != SUPRA_NORM_COUNT && c->normalize != SUPRA_NORM_NONE) return fail(SUPRA_E_PARAM, "normalize");
+  if (c->interpolation != SUPRA_INTERP_LINEAR && c->interpolation != SUPRA_INTERP_NEAREST)
+    return fail(SUPRA_E_PARAM, "interpolation must be LINEAR or NEAREST (S:125)");
   if (c->fir_taps < 1 || c->fir_taps > 129 || c->fir_taps % 2 == 0)
     return fail(SUPRA_E_PARAM, "fir_taps must be odd in [1, 129] (S:196)");
   if (c->decimation != 1) return fail(SUPRA_E_PARAM, "decimation must be 1 in this version");
@@ -783,7 +785,10 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.ncount = h->d_ncount;
   a.line_dir = h->d_line_dir;
   a.line_event = h->d_line_event;
-  a.t0fs = (float)(c.t0_s * c.sample_frequency_hz);
+  // nearest-sample lookup x~[floor(tau + 1/2)]: shift tau by 1/2, drop the fraction
+  const bool nearest = c.interpolation == SUPRA_INTERP_NEAREST;
+  a.t0fs = (float)(c.t0_s * c.sample_frequency_hz + (nearest ? 0.5 : 0.0));
+  a.fr_scale = nearest ? 0.f : 1.f;
   a.win_a = c.window == SUPRA_WIN_HANN ? 0.5f : (c.window == SUPRA_WIN_HAMMING ? 0.54f : 1.0f);
   a.win_b = c.window == SUPRA_WIN_HANN ? 0.5f : (c.window == SUPRA_WIN_HAMMING ? 0.46f : 0.0f);
   a.normalize = c.normalize;

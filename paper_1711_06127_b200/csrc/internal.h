@@ -62,7 +62,8 @@ struct DasArgs {
   const uint16_t* ncount;      // [G][S]: N(k) = #entries with kenter <= k
   const float4* line_dir;      // [L] (dx, dy, dz, 0)
   const int32_t* line_event;   // [L]
-  float t0fs;                  // t0 * fs (samples)
+  float t0fs;                  // t0 * fs (samples); + 1/2 for nearest-sample lookup
+  float fr_scale;              // 1: linear interpolation; 0: nearest sample (x~[floor(tau + 1/2)])
   float win_a, win_b;          // w = a + b cos(pi u)
   int normalize;               // 0 count, 1 none
   // outputs

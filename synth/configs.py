@@ -17,6 +17,7 @@ from typing import Optional
 import numpy as np
 
 WIN_RECT, WIN_HANN, WIN_HAMMING = 0, 1, 2
+INTERP_LINEAR, INTERP_NEAREST = 0, 1
 NORM_COUNT, NORM_NONE = 0, 1
 REF_FRAME_MAX, REF_FIXED = 0, 1
 T_I16, T_F32, T_U8 = 0, 1, 2
@@ -70,6 +71,8 @@ class Workload:
     # receive channel map [E][channels] -> element (-1 unused); None = one
     # channel per element ("only 64 channels usable")
     channel_element: Optional[np.ndarray] = None
+    # fractional-delay lookup: 0 linear, 1 nearest (reading #32)
+    interpolation: int = 0
     dynamic_range_db: float = 50.0
     reference_mode: int = REF_FRAME_MAX
     reference_value: float = 1.0

@@ -72,6 +72,7 @@ def _create(w, **over):
     ("fir_taps", 64), ("fir_taps", 0), ("dynamic_range_db", 0.0), ("samples_per_channel", 1020),
     ("pitch_x_mm", -0.3), ("window", 7), ("decimation", 2), ("abi_version", 99),
     ("max_frames_per_call", 0), ("demod_bandwidth_hz", 80e6), ("fov_x_deg", 180.0),
+    ("interpolation", 2),
 ])
 def test_param_errors(field, value):
     w = configs.c3() if field == "fov_x_deg" else configs.c1()

@@ -237,6 +237,9 @@ def _brute_force_das(w, raw):
             a = np.where((i0 >= 0) & (i0 < w.S), xp[ch, np.clip(i0, 0, w.S + 1)], 0.0)
             b = np.where((i0 + 1 >= 0) & (i0 + 1 < w.S), xp[ch, np.clip(i0 + 1, 0, w.S + 1)], 0.0)
             v = (1 - f) * a + f * b
+            if getattr(w, "interpolation", 0) == 1:       # nearest (reading #32)
+                i1 = np.floor(tau + 0.5).astype(int)
+                v = np.where((i1 >= 0) & (i1 < w.S), xp[ch, np.clip(i1, 0, w.S + 1)], 0.0)
             u = rho / (z / (2 * w.f_number)) if z > 0 else np.zeros_like(rho)
             wt = 0.5 * (1 + np.cos(np.pi * u))
             out[l, k] = np.sum((wt * v)[mem]) / mem.sum()
@@ -336,3 +339,40 @@ def test_bruteforce_walking_aperture_multiline_S570():
     a = oracle.das(w, raw)
     b = _brute_force_das(w, raw)
     assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
+
+
+
+@pytest.mark.parametrize("kind", ["linear", "phased"])
+def test_bruteforce_nearest_interpolation_S125(kind):
+    rng = np.random.default_rng(21)
+    if kind == "linear":
+        w = tiny_linear(n_el=16, S=256, interpolation=1)
+    else:
+        o, d = configs.phased_lines(12, 50.0)
+        ev = (np.arange(12) % 8).astype(np.int32)
+        w = configs.Workload("tp", 16, 1, 0.22, 0.22, 3.5e6, 8, 256, 12, 1, o, d, ev,
+                             np.zeros((8, 3)), configs.SC_SECTOR_2D, (8, 1, 8), (0, 0, 0),
+                             (0.1, 0.1, 0.1), fov_x_deg=50.0, interpolation=1)
+    raw = rng.integers(-3000, 3000, (w.num_events, w.C, w.S)).astype(np.int16)
+    a = oracle.das(w, raw)
+    b = _brute_force_das(w, raw)
+    assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
+    # and it is not the linear result
+    assert np.max(np.abs(a - oracle.das(w.replace(interpolation=0), raw))) > 1e-3 * np.max(np.abs(b))
+
+
+def test_nearest_picks_rounded_sample_single_element():
+    # one element, one line through it: tau(k) = k + |q|... here q = 0, so
+    # tau = k exactly and both lookups return x[k]; with t0 = 0.4 samples the
+    # nearest lookup still returns x[k] (k + 0.4 rounds down) and with t0 =
+    # 0.6 it returns x[k + 1] (ties and above round up)
+    w = tiny_linear(n_el=1, S=64, window=configs.WIN_RECT, normalize=configs.NORM_NONE, interpolation=1)
+    w = w.replace(num_lines_x=1, line_origin_mm=np.zeros((1, 3)), line_direction=np.array([[0, 0, 1.0]]),
+                  line_event=np.zeros(1, np.int32), num_events=1, tx_origin_mm=np.zeros((1, 3)))
+    x = np.arange(64, dtype=np.int16)[None, None, :] * 3
+    fs = w.fs_hz
+    rf4 = oracle.das(w.replace(t0_s=0.4 / fs), x)[0]
+    rf6 = oracle.das(w.replace(t0_s=0.6 / fs), x)[0]
+    k = np.arange(10, 60)
+    assert np.array_equal(rf4[k], 3.0 * k)
+    assert np.array_equal(rf6[k], 3.0 * (k + 1))

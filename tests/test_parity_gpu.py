@@ -64,6 +64,8 @@ def test_c1_point_target_full_chain():
     dict(t0_s=-2.5e-7),
     dict(t0_s=3e-7, fir_taps=33),
     dict(reference_mode=configs.REF_FIXED, reference_value=5000.0),
+    dict(interpolation=configs.INTERP_NEAREST),
+    dict(interpolation=configs.INTERP_NEAREST, window=configs.WIN_HAMMING, t0_s=1e-7),
 ])
 def test_c1_variants(over):
     w = configs.c1(**over)
@@ -377,3 +379,14 @@ def test_table1_batch_and_scan_conversion():
     valid_g, idx_g = bf.sc_indices()
     assert np.array_equal(valid_g, valid_o)
     assert np.array_equal(idx_g[valid_o.astype(bool)], idx_o[valid_o.astype(bool)])
+
+
+
+def test_c2_nearest_interpolation_batch():
+    w = configs.c2(interpolation=configs.INTERP_NEAREST)
+    F = 2
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    rf_g, y_g = run_gpu(bf, raw, F)
+    e_rf, e_db, _, _ = check_frame(w, raw[1].cpu().numpy(), rf_g[1], y_g[1])
+    assert e_rf <= RF_TOL and e_db <= DB_TOL, (e_rf, e_db)
