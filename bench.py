@@ -340,6 +340,7 @@ def main():
         cpu_baseline = {"value": r, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample}
     if not args.no_secondary:
         secondary = secondary_3d(local, world, rank)
+        secondary.update(secondary_paper3d(local, world, rank))
         secondary.update(secondary_table1(local, world, rank))
 
     if rank == 0:
@@ -430,6 +431,54 @@ def secondary_3d(dev_index: int, world: int = 1, rank: int = 0, vols: int = 8):
                          if world > 1 else "single GPU"}
     bf.close()
     del raw, li, img, sv
+    torch.cuda.empty_cache()
+    return out
+
+
+def secondary_paper3d(dev_index: int, world: int = 1, rank: int = 0, vols: int = 4):
+    """Volumes/s on the paper's own 3D shape (C4p: 32x32 matrix probe through
+    384 channels, 32x16 scanlines, 60 deg, 70 mm, 0.175 mm pyramid output
+    401x401x402 u8): "C4p_single" one volume per
+    call, "C4p_stream" ``vols`` volumes per call per rank (weak scaling).
+    DAS + envelope/log + scan conversion, device-timed, inputs resident."""
+    import torch
+    import torch.distributed as dist
+    import synth
+    from synth import configs
+    from paper_1711_06127_b200 import SupraBF
+    dev = torch.device(f"cuda:{dev_index}")
+    w = configs.c4p(sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
+    raw = torch.empty((vols, w.num_events, w.C, w.S), dtype=torch.int16, device=dev)
+    synth.channel_data_gpu(w, raw[0], realisation=0)
+    for v in range(1, vols):
+        raw[v].copy_(raw[0])
+    bf = SupraBF(w, device=dev_index, max_frames=vols)
+    li, img = bf.empty_line_img(vols), bf.empty_img(vols)
+    out = {}
+    for n, key, reps in ((1, "C4p_single", 10), (vols, "C4p_stream", 5)):
+        def call():
+            bf.beamform(raw, n, line_img=li)
+            bf.scanconvert(li, n, img)
+        for _ in range(2):
+            call()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            call()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        out[key] = {"value": n * world * 1000.0 / ms, "unit": "volumes/s", "ms_per_call": ms,
+                    "volumes_per_call_per_rank": n, "scaling": "weak",
+                    "paper_gtx1080_vol_s_context": round(1000 / 27.49, 1)}
+    bf.close()
+    del raw, li, img
     torch.cuda.empty_cache()
     return out
 

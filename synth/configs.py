@@ -256,10 +256,36 @@ def table1(tx_events: int = 128, multiline: int = 2, frames: int = 1, **kw) -> W
     return w.replace(**kw) if kw else w
 
 
+def c4p(volumes: int = 1, **kw) -> Workload:
+    """The paper's own 3D row:
+    32 x 32 matrix probe (0.3 mm, 7 MHz) driven through 384 channels,
+    32 x 16 = 512 scanlines over a 60 x 60 deg field of view, 70 mm depth
+    (S = 3648 samples = 70.2 mm at 40 MHz, a multiple of 32), one transmit
+    per line; 0.175 mm isotropic pyramid scan conversion (401 x 401 x 402).
+    The 384 channels are the 12 central element rows (j = 10 .. 21, all 32
+    columns) for every event (reading #33: the paper does not say which
+    elements its 384-channel system drives)."""
+    o, d = phased_lines(32, 60.0, 16, 60.0)
+    E = 512
+    ev = np.arange(E, dtype=np.int32)
+    S = 3648
+    chm = np.tile((10 * 32 + np.arange(384)).astype(np.int32), (E, 1))
+    sp = 0.175
+    rmax = (S - 1) * dr_mm()
+    half = int(math.floor(rmax * math.sin(math.radians(30.0)) / sp))
+    nz = int(math.floor(rmax / sp)) + 1
+    w = Workload("C4p", 32, 32, 0.3, 0.3, 7e6, E, S, 32, 16, o, d, ev, tx_origins(o, ev, E),
+                 SC_PYRAMID_3D, (2 * half + 1, 2 * half + 1, nz), (-half * sp, -half * sp, 0.0),
+                 (sp, sp, sp), fov_x_deg=60.0, fov_y_deg=60.0, noise_db=-40.0, frames=volumes,
+                 channel_element=chm)
+    return w.replace(**kw) if kw else w
+
+
 CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4a": lambda **k: c4("a", **k),
            "C4b": lambda **k: c4("b", **k), "C2b": lambda **k: c2("b", **k),
            "T1_64_1": lambda **k: table1(64, 1, **k), "T1_64_2": lambda **k: table1(64, 2, **k),
-           "T1_128_1": lambda **k: table1(128, 1, **k), "T1_128_2": lambda **k: table1(128, 2, **k)}
+           "T1_128_1": lambda **k: table1(128, 1, **k), "T1_128_2": lambda **k: table1(128, 2, **k),
+           "C4p": c4p}
 
 
 # ------------------------------------------------------------- scatterers
@@ -302,6 +328,16 @@ def scatterers(w: Workload, realisation: int = 0) -> np.ndarray:
         for i, zz in enumerate(range(10, 80, 10)):
             s[n + i] = [0, 0, zz, 20]
         return s
+    if name == "C4p":
+        # wire grid over the paper's 70 mm pyramid
+        pts = []
+        for tx in (-20, 0, 20):
+            for ty in (-20, 0, 20):
+                for r in (10, 25, 40, 55, 68):
+                    a, b = math.radians(tx), math.radians(ty)
+                    pts.append([r * math.sin(a), r * math.cos(a) * math.sin(b),
+                                r * math.cos(a) * math.cos(b), 1.0])
+        return np.array(pts)
     if name.startswith("C4"):
         pts = []
         for tx in (-20, -10, 0, 10, 20):

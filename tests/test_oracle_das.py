@@ -376,3 +376,16 @@ def test_nearest_picks_rounded_sample_single_element():
     k = np.arange(10, 60)
     assert np.array_equal(rf4[k], 3.0 * k)
     assert np.array_equal(rf6[k], 3.0 * (k + 1))
+
+
+def test_paper_3d_shape_P228_P337():
+    # P:228 "512 (32 x 16) scanlines over a field of view of 60 deg", 70 mm
+    # depth; P:347 384 channels; P:337 0.175 mm isotropic output
+    w = configs.c4p()
+    assert w.L == 512 and (w.num_lines_x, w.num_lines_y) == (32, 16)
+    assert w.C == 384 and (w.S - 1) * configs.dr_mm() >= 70.0
+    assert np.all(np.diff(np.sort(w.channel_element[0])) > 0)            # distinct elements
+    th = np.degrees(np.arctan2(w.line_direction[:, 0],
+                               np.hypot(w.line_direction[:, 1], w.line_direction[:, 2])))
+    assert abs(th.max() - 30.0) < 1e-9 and abs(th.min() + 30.0) < 1e-9   # S:66 endpoints
+    assert w.out_spacing_mm == (0.175, 0.175, 0.175)

@@ -390,3 +390,20 @@ def test_c2_nearest_interpolation_batch():
     rf_g, y_g = run_gpu(bf, raw, F)
     e_rf, e_db, _, _ = check_frame(w, raw[1].cpu().numpy(), rf_g[1], y_g[1])
     assert e_rf <= RF_TOL and e_db <= DB_TOL, (e_rf, e_db)
+
+
+# ------------------------------ the paper's 3D shape (f4)
+def test_c4p_paper_3d_sampled_lines_and_indices():
+    w = configs.c4p()
+    raw = raw_frames(w, 1)
+    bf = SupraBF(w)
+    rf_g, _ = run_gpu(bf, raw, 1)
+    rng = np.random.default_rng(17)
+    lines = np.sort(np.concatenate([[0, 255, 256, 511], rng.choice(512, 8, replace=False)])).astype(np.int32)
+    e_rf, _, _, _ = check_frame(w, raw[0].cpu().numpy(), rf_g[0], None, lines=lines)
+    assert e_rf <= RF_TOL, e_rf
+    valid_o, idx_o, _ = oracle.sc_table(w)
+    valid_g, idx_g = bf.sc_indices()
+    assert np.array_equal(valid_g, valid_o)
+    v = valid_o.astype(bool)
+    assert np.array_equal(idx_g[v], idx_o[v])
