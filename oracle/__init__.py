@@ -228,8 +228,10 @@ def to_u8(y):
 
 def _sc_params(cfg):
     o = np.asarray(cfg.line_origin_mm, np.float64)
-    return _ScParams(cfg.sc_kind, cfg.num_lines_x, cfg.num_lines_y, cfg.S,
-                     dr_mm(cfg.c_mps, cfg.fs_hz), float(o[0, 0]), float(o[-1, 0]),
+    # the line image holds S // d samples spaced d * dr (decimation d)
+    d = int(getattr(cfg, "decimation", 1))
+    return _ScParams(cfg.sc_kind, cfg.num_lines_x, cfg.num_lines_y, cfg.S // d,
+                     dr_mm(cfg.c_mps, cfg.fs_hz) * d, float(o[0, 0]), float(o[-1, 0]),
                      cfg.fov_x_deg, cfg.fov_y_deg, cfg.out_dims[0], cfg.out_dims[1],
                      cfg.out_dims[2], (C.c_double * 3)(*cfg.out_origin_mm),
                      (C.c_double * 3)(*cfg.out_spacing_mm))

@@ -184,6 +184,7 @@ class SupraBF:
         self.h = h
         self.L = w.num_lines_x * w.num_lines_y
         self.S = w.S
+        self.Sd = w.S // max(1, w.decimation)   # line-image samples
         self.max_frames = max_frames
 
     # -- entry points ------------------------------------------------------
@@ -247,7 +248,7 @@ class SupraBF:
     def empty_line_img(self, frames: int):
         import torch
         dt = torch.uint8 if self.w.line_output_type == T_U8 else torch.float32
-        return torch.empty((frames, self.L, self.S), dtype=dt, device=f"cuda:{self.device}")
+        return torch.empty((frames, self.L, self.Sd), dtype=dt, device=f"cuda:{self.device}")
 
     def empty_rf(self, frames: int):
         import torch

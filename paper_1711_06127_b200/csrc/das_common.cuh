@@ -205,11 +205,17 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
   for (int o = 0; o < 4; o++) {
     const int k = o0 + o;
     if (k >= o_end) break;
+    // decimation: only k = dec q is kept, at line-image index q
+    int kq = k;
+    if (a.dec > 1) {
+      kq = k / a.dec;
+      if (kq * a.dec != k || kq >= a.Sd) continue;
+    }
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const int f = fg0 + q;
       if (q >= FB || f >= a.F) break;
-      const size_t out = ((size_t)f * a.L + line) * a.S + k;
+      const size_t out = ((size_t)f * a.L + line) * a.Sd + kq;
       const float e = env[o][q];
       if (a.ref_fixed) {
         const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(e), a.log_k0), 0.f), 1.f) : 0.f;

@@ -29,9 +29,10 @@ __global__ void __launch_bounds__(256) envlog_kernel(const EnvArgs a) {
   if (threadIdx.x == 0) smax = 0u;
   __syncthreads();
   float m = 0.f;
-  for (int k = threadIdx.x; k < S; k += blockDim.x) {
+  for (int q = threadIdx.x; q < a.Sd; q += blockDim.x) {  // decimation keeps k = dec q
+    const int k = q * a.dec;
     const float env = compound_at(rfs + P + k, cs, a.band_w, a.nbands, P);
-    const size_t o = ((size_t)f * a.L + line) * S + k;
+    const size_t o = ((size_t)f * a.L + line) * a.Sd + q;
     if (a.ref_fixed) {
       const float y = env > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(env), a.log_k0), 0.f), 1.f) : 0.f;
       if (a.y_type == SUPRA_T_U8) ((uint8_t*)a.y_out)[o] = (uint8_t)floorf(255.f * y + 0.5f);

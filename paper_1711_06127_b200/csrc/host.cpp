@@ -56,6 +56,7 @@ struct DeviceGuard {
 struct supra_bf {
   supra_bf_config cfg{};
   int L = 0, C = 0, S = 0, E = 0, G = 0;
+  int dec = 1, Sd = 0;  // envelope decimation and line-image samples S / dec
   int ntiles = 0, entries_per_group = 0;
   int frames_per_cta = 1;
   size_t das_smem = 0;
@@ -178,7 +179,8 @@ supra_status validate(const supra_bf_config* c) {
     return fail(SUPRA_E_PARAM, "interpolation must be LINEAR or NEAREST (S:125)");
   if (c->fir_taps < 1 || c->fir_taps > 129 || c->fir_taps % 2 == 0)
     return fail(SUPRA_E_PARAM, "fir_taps must be odd in [1, 129] (S:196)");
-  if (c->decimation != 1) return fail(SUPRA_E_PARAM, "decimation must be 1 in this version");
+  if (c->decimation < 1 || c->samples_per_channel / c->decimation < 2)
+    return fail(SUPRA_E_PARAM, "decimation must be >= 1 with samples_per_channel / decimation >= 2 (S:224)");
   double fd = c->demod_frequency_hz, bw = c->demod_bandwidth_hz;
   if (!(bw > 0) || !(fd - bw / 2 > 0) || !(fd + bw / 2 < c->sample_frequency_hz / 2))
     return fail(SUPRA_E_PARAM, "demodulation band must lie inside (0, fs/2) (S:188)");
@@ -454,8 +456,9 @@ void sc_axis(double u, int L, int32_t* i0, double* f) {
 supra_status build_sc_tables(supra_bf* h) {
   const supra_bf_config& c = h->cfg;
   const int nx = c.out_dims[0], ny = c.out_dims[1], nz = c.out_dims[2];
-  const int Lx = c.num_lines_x, Ly = c.num_lines_y, S = h->S;
-  const double dr = h->dr_mm;
+  // the line image holds S / dec samples spaced dec * dr
+  const int Lx = c.num_lines_x, Ly = c.num_lines_y, S = h->Sd;
+  const double dr = h->dr_mm * h->dec;
   int64_t nvalid = 0;
   cudaError_t e = cudaSuccess;
   if (c.sc_kind == SUPRA_SC_LINEAR_2D) {
@@ -706,6 +709,8 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   h->L = cfg->num_lines_x * cfg->num_lines_y;
   h->C = cfg->num_channels > 0 ? cfg->num_channels : cfg->elements_x * cfg->elements_y;
   h->S = cfg->samples_per_channel;
+  h->dec = cfg->decimation;
+  h->Sd = h->S / h->dec;
   h->E = cfg->num_events;
   h->dr_mm = 1000.0 * cfg->speed_of_sound_mps / (2.0 * cfg->sample_frequency_hz);
   h->s_per_mm = cfg->sample_frequency_hz / (1000.0 * cfg->speed_of_sound_mps);
@@ -777,6 +782,8 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.E = h->E;
   a.C = h->C;
   a.S = h->S;
+  a.Sd = h->Sd;
+  a.dec = h->dec;
   a.L = h->L;
   a.entries_per_group = h->entries_per_group;
   a.line_group = h->d_line_group;
@@ -863,7 +870,7 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   if (s != SUPRA_OK || !line_img || a.ref_fixed || env_ext) return s;
   FinalizeArgs fa{};
   fa.env = a.env_out;
-  fa.per_frame = (long long)h->L * h->S;
+  fa.per_frame = (long long)h->L * h->Sd;
   fa.frame_stride = fa.per_frame;
   fa.F = frames;
   fa.frame_max = h->d_frame_max;
@@ -944,9 +951,9 @@ supra_status supra_bf_log_compress(supra_bf_t h, const float* env, int32_t frame
   fill_log(h, fixed, k1, k0);
   FinalizeArgs fa{};
   fa.env = env;
-  fa.per_frame = (long long)line_count * h->S;
-  fa.frame_stride = (long long)h->L * h->S;
-  fa.offset = (long long)line_first * h->S;
+  fa.per_frame = (long long)line_count * h->Sd;
+  fa.frame_stride = (long long)h->L * h->Sd;
+  fa.offset = (long long)line_first * h->Sd;
   fa.F = frames;
   fa.frame_max = fixed ? nullptr : (const unsigned*)frame_max;
   fa.fixed_ref = (float)c.reference_value;
@@ -974,6 +981,8 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames
   a.F = frames;
   a.L = h->L;
   a.S = h->S;
+  a.Sd = h->Sd;
+  a.dec = h->dec;
   a.fir = h->d_fir;
   a.fir_taps = c.fir_taps;
   a.nbands = h->nbands;
@@ -992,7 +1001,7 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames
   if (s != SUPRA_OK || a.ref_fixed) return s;
   FinalizeArgs fa{};
   fa.env = a.env_out;
-  fa.per_frame = (long long)h->L * h->S;
+  fa.per_frame = (long long)h->L * h->Sd;
   fa.frame_stride = fa.per_frame;
   fa.F = frames;
   fa.frame_max = h->d_frame_max;
@@ -1021,7 +1030,7 @@ supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t fr
   a.F = frames;
   a.Lx = c.num_lines_x;
   a.Ly = c.num_lines_y;
-  a.S = h->S;
+  a.S = h->Sd;  // line-image samples (S / decimation)
   a.nx = c.out_dims[0];
   a.ny = c.out_dims[1];
   a.nz = c.out_dims[2];
@@ -1042,7 +1051,7 @@ supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t fr
   a.is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
   // bulk-copy staging of the slab: 16-byte aligned line segments
   a.slab_tma = (c.sc_kind == SUPRA_SC_LINEAR_2D && h->sc_tiled && c.line_output_type == SUPRA_T_F32 &&
-                (h->S % 4) == 0 && ((uintptr_t)line_img & 15) == 0)
+                (h->Sd % 4) == 0 && ((uintptr_t)line_img & 15) == 0)
                    ? 1
                    : 0;
   cudaStream_t st = (cudaStream_t)stream;

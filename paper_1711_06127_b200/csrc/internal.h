@@ -51,6 +51,7 @@ struct __align__(16) DasEntry {
 struct DasArgs {
   const int16_t* raw;      // [F][E][C][S]
   int F, E, C, S, L;
+  int dec, Sd;             // envelope decimation: line image [F][L][Sd], Sd = S / dec, keeps k = dec q
   int entries_per_group;   // row stride of `entries`
   int line0, nlines;           // lines [line0, line0 + nlines) of every frame are beamformed
   int fbase, Fmap;             // frames [fbase, fbase + Fmap) of the call, = frames [0, Fmap) of the tensor map
@@ -97,6 +98,7 @@ struct DasArgs {
 struct EnvArgs {  // standalone epilogue on an RF buffer
   const float* rf;
   int F, L, S;
+  int dec, Sd;         // line image [F][L][Sd], k = dec q
   const float2* fir;   // [nbands][T]
   int fir_taps;
   int nbands;

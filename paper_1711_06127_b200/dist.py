@@ -68,7 +68,8 @@ class ShardedVolume:
          rank 0 (or on any rank) from the full line image.
     No input exchange: the blocks read disjoint events.  ``bf`` is a SupraBF
     handle (or any object with beamform_lines / log_compress of the same
-    signature); ``y_dtype`` is the line-image dtype of its config."""
+    signature); ``y_dtype`` is the line-image dtype of its config and ``S``
+    its line-image samples per line (samples_per_channel / decimation)."""
 
     def __init__(self, bf, L: int, S: int, y_dtype: torch.dtype, device, align: int = 1,
                  fixed_reference: bool = False):

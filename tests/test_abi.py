@@ -70,7 +70,7 @@ def _create(w, **over):
 @pytest.mark.parametrize("field,value", [
     ("speed_of_sound_mps", 999.0), ("speed_of_sound_mps", 2001.0), ("f_number", 0.0),
     ("fir_taps", 64), ("fir_taps", 0), ("dynamic_range_db", 0.0), ("samples_per_channel", 1020),
-    ("pitch_x_mm", -0.3), ("window", 7), ("decimation", 2), ("abi_version", 99),
+    ("pitch_x_mm", -0.3), ("window", 7), ("decimation", 0), ("decimation", 1024), ("abi_version", 99),
     ("max_frames_per_call", 0), ("demod_bandwidth_hz", 80e6), ("fov_x_deg", 180.0),
     ("interpolation", 2),
 ])

@@ -178,3 +178,23 @@ def test_pyramid_valid_count_C4():
     diff = int(np.sum(valid.reshape(n, n, n).astype(bool) != geo))
     assert diff <= 8, diff                     # exact-boundary ties only
     assert abs(int(valid.sum()) - int(geo.sum())) <= 8
+
+
+@pytest.mark.parametrize("dec", [2, 3])
+def test_decimated_line_image_depth_axis_S224(dec):
+    # with decimation d the line image holds k = d q at depth d q dr, so a
+    # line image y[q] = d q (the full-rate sample index) scan-converts to
+    # Z / dr exactly (linear interpolation reproduces linear functions)
+    w = small_linear().replace(decimation=dec)
+    Sd = w.S // dec
+    q = np.arange(Sd)[None, :].repeat(w.L, 0).astype(float)
+    img, mask = oracle.scan_convert(w, dec * q)
+    Z = np.arange(w.out_dims[2]) * w.out_spacing_mm[2]
+    expect = (Z / configs.dr_mm())[:, None].repeat(w.out_dims[0], 1)
+    m = mask[:, 0, :] == 1
+    assert m.any()
+    assert np.max(np.abs(img[:, 0, :][m] - expect[m])) < 1e-9
+    # the valid depth range ends at the last decimated sample (S:224 floor)
+    zmax = (Sd - 1) * dec * configs.dr_mm()
+    rows = np.where(m.any(1))[0]
+    assert Z[rows].max() <= zmax + 1e-12 and Z[rows.max() + 1] > zmax if rows.max() + 1 < len(Z) else True

@@ -407,3 +407,45 @@ def test_c4p_paper_3d_sampled_lines_and_indices():
     assert np.array_equal(valid_g, valid_o)
     v = valid_o.astype(bool)
     assert np.array_equal(idx_g[v], idx_o[v])
+
+
+# ----------------------------------------- envelope decimation (f4)
+@pytest.mark.parametrize("dec", [2, 3])
+def test_c1_decimation_full_chain(dec):
+    w = configs.c1(decimation=dec)
+    raw = raw_frames(w, 1)
+    bf = SupraBF(w)
+    rf_g, y_g = run_gpu(bf, raw, 1)
+    assert y_g.shape == (1, w.L, w.S // dec)
+    rf_o, env_o = oracle_chain(w, raw[0].cpu().numpy())
+    assert rf_err(rf_g[0], rf_o) <= RF_TOL
+    y_o, _ = oracle.log_compress(env_o, w.dynamic_range_db)
+    assert db_err(y_g[0], y_o) <= DB_TOL
+    # standalone epilogue: bitwise the fused result
+    li2 = bf.empty_line_img(1)
+    bf.envelope_log(torch.from_numpy(rf_g).cuda(), 1, li2)
+    torch.cuda.synchronize()
+    assert np.array_equal(li2.cpu().numpy(), y_g)
+    # scan conversion of the decimated line image: bit-exact indices, values
+    img, mask = bf.empty_img(1), bf.empty_mask()
+    bf.scanconvert(torch.from_numpy(y_g).cuda(), 1, img, mask)
+    torch.cuda.synchronize()
+    img_o, mask_o = oracle.scan_convert(w, y_o)
+    assert np.array_equal(mask.cpu().numpy(), mask_o)
+    assert db_err(img.cpu().numpy()[0], img_o) <= DB_TOL
+    valid_o, idx_o, _ = oracle.sc_table(w)
+    valid_g, idx_g = bf.sc_indices()
+    v = valid_o.astype(bool)
+    assert np.array_equal(valid_g, valid_o) and np.array_equal(idx_g[v], idx_o[v])
+
+
+def test_c2_decimation_batch():
+    w = configs.c2(decimation=4, line_output_type=configs.T_U8)
+    F = 3
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    rf_g, y_g = run_gpu(bf, raw, F)
+    rf_o, env_o = oracle_chain(w, raw[1].cpu().numpy())
+    assert rf_err(rf_g[1], rf_o) <= RF_TOL
+    y_o, _ = oracle.log_compress(env_o, w.dynamic_range_db)
+    assert np.max(np.abs(y_g[1].astype(int) - oracle.to_u8(y_o).astype(int))) <= 1
