@@ -281,6 +281,33 @@ def c4p(volumes: int = 1, **kw) -> Workload:
     return w.replace(**kw) if kw else w
 
 
+def wire_phantom(depths_mm, x_mm=0.0, reflectivity=1.0) -> np.ndarray:
+    """SPEC wire_phantom (the paper's water-tank wire target at
+    5, 10, 15, 20, 25 mm): one unit-reflectivity scatterer per
+    depth, centred laterally.  [n][4] = (x, y, z, reflectivity)."""
+    d = np.asarray(list(depths_mm), np.float64)
+    out = np.zeros((len(d), 4))
+    out[:, 0], out[:, 2], out[:, 3] = x_mm, d, reflectivity
+    return out
+
+
+def psf_linear(half_width_mm: float = 3.0, n_lines: int = 201, S: int = 1408, **kw) -> Workload:
+    """PSF measurement layout (f3; Fig. 4): the 128-element 0.3 mm
+    7 MHz linear probe with all 128 channels, ``n_lines`` lines
+    evenly spaced over +-half_width_mm around the array centre (dense
+    lateral sampling, 0.03 mm for the default), one transmit per line from
+    the line origin, S samples (27.1 mm for the default)."""
+    xs = np.linspace(-half_width_mm, half_width_mm, n_lines)
+    o, d = linear_lines(xs)
+    ev = np.arange(n_lines, dtype=np.int32)
+    s = 0.0225
+    nx = int(round(2 * half_width_mm / s)) + 1
+    nz = int(math.floor((S - 1) * dr_mm() / s)) + 1
+    w = Workload("PSF", 128, 1, 0.3, 0.3, 7e6, n_lines, S, n_lines, 1, o, d, ev, tx_origins(o, ev, n_lines),
+                 SC_LINEAR_2D, (nx, 1, nz), (-half_width_mm, 0.0, 0.0), (s, s, s))
+    return w.replace(**kw) if kw else w
+
+
 CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4a": lambda **k: c4("a", **k),
            "C4b": lambda **k: c4("b", **k), "C2b": lambda **k: c2("b", **k),
            "T1_64_1": lambda **k: table1(64, 1, **k), "T1_64_2": lambda **k: table1(64, 2, **k),
