@@ -519,7 +519,19 @@ supra_status build_sc_tables(supra_bf* h) {
     }
     int maxnl = 0;
     for (int v : cnl) maxnl = std::max(maxnl, v);
-    h->sc_tiled = (maxnl <= kScMaxLines && h->slab_k + 3 <= kScMaxK) ? 1 : 0;  // else direct kernel
+    // per 32-column warp group: lines touched (the tiled kernel's per-warp depth lerp)
+    int maxwl = 0;
+    for (int w0 = 0; w0 < nx; w0 += 32) {
+      int lo = -1, hi = -1;
+      for (int ix = w0; ix < std::min(nx, w0 + 32); ix++) {
+        int i0 = h->h_ax[ix].i0;
+        if (i0 < 0) continue;
+        if (lo < 0 || i0 < lo) lo = i0;
+        if (i0 + 1 > hi) hi = i0 + 1;
+      }
+      if (lo >= 0) maxwl = std::max(maxwl, hi - lo + 1);
+    }
+    h->sc_tiled = (maxnl <= kScMaxLines && h->slab_k + 3 <= kScMaxK && maxwl <= kScWarpLinesMax - 1) ? 1 : 0;  // else direct kernel
     h->sc_box_l = std::max(1, maxnl);
     h->sc_box_k = std::min(kScMaxK, (h->slab_k + 3 + 3) & ~3);   // 16-byte rows, + alignment slack
     if ((e = upload(&h->d_blk_kmin, kmin)) != cudaSuccess || (e = upload(&h->d_col_l0, cl0)) != cudaSuccess ||

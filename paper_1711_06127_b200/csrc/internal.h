@@ -127,6 +127,8 @@ struct FinalizeArgs {  // env -> y with a per-frame (or fixed) reference
 // staged slab holds at most kScMaxLines lines x kScMaxK samples (checked at
 // create: the tile's columns must span <= kScMaxLines - 1 line pitches).
 constexpr int kScRows = 32;
+// lines the 32 columns of one warp may touch (+1), checked at create
+constexpr int kScWarpLinesMax = 11;
 constexpr int kScMaxLines = 64;
 constexpr int kScMaxK = 64;
 

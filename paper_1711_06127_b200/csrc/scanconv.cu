@@ -27,12 +27,6 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
                : "memory");
 }
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-
 __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) {
   if (type == SUPRA_T_U8) ((uint8_t*)p)[i] = (uint8_t)floorf(255.f * v + 0.5f);
   else ((float*)p)[i] = v;
@@ -41,21 +35,30 @@ __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) 
 }  // namespace
 
 // Linear 2D, tiled and separable: one CTA per (256 output columns x
-// kScRows output rows, frame); one thread per column.  Because u depends
-// only on x and v only on z (reading #21), the bilinear blend factors into a
-// depth lerp per (row, line) followed by a lateral lerp per pixel:
+// kScRows output rows) and a group of `fpc` frames; one thread per column.
+// Because u depends only on x and v only on z (reading #21), the bilinear
+// blend factors into a depth lerp per (row, line) followed by a lateral lerp
+// per pixel:
 //   t[r][l] = lerp(y[l][k0], y[l][k0+1], fz(r)),
 //   out[r][x] = lerp(t[r][i0], t[r][i0+1], fx(x)).
 // The slab of the line image the tile touches (lines [l0, l0+nl) x ks
 // samples from the row block's smallest k0, both host-computed) is staged in
-// shared memory with one 1-D bulk copy (TMA) per line.
+// shared memory with one 1-D bulk copy (TMA) per line.  The CTA walks its
+// frames with two slab buffers (the next frame's copies in flight while the
+// current one is blended; tables read once per CTA).  Each warp does the
+// depth lerp only for the few lines its 32 columns touch (lane = output
+// row) into its own small buffer, so the two phases need only __syncwarp;
+// a per-buffer "empty" mbarrier (8 warp arrivals) gates the refill.
+constexpr int kScWarpLines = kScWarpLinesMax + 1;  // + the zero pair
 template <bool U8OUT>
-__global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
-  __shared__ __align__(128) float slab[kScMaxLines * kScMaxK];
-  __shared__ float tz[kScRows * (kScMaxLines + 2)];
+__global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a, int fpc) {
+  __shared__ __align__(128) float slab[2][kScMaxLines * kScMaxK];
+  constexpr int TZS = kScWarpLines + 1;  // odd row stride: conflict-free row writes
+  __shared__ float tzw[8][kScRows * TZS];
   __shared__ ScAxis saz[kScRows];
-  __shared__ __align__(8) uint64_t bar;
-  const int cb = blockIdx.x, rb = blockIdx.y, f = blockIdx.z;
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  const int cb = blockIdx.x, rb = blockIdx.y;
+  const int fbeg = blockIdx.z * fpc, fend = min(a.F, fbeg + fpc);
   const int x = cb * 256 + threadIdx.x;
   const int z0 = rb * kScRows;
   const int ks = a.slab_k;
@@ -63,92 +66,130 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a) {
   const int l0 = a.col_l0[cb], nl = a.col_nl[cb];
   const int Lx = a.Lx, S = a.S, nx = a.nx;
   const int rows = min(kScRows, a.nz - z0);
-  const size_t fbase = (size_t)f * Lx * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool use_tma = a.in_type == SUPRA_T_F32 && a.slab_tma;
   const int kstride = use_tma ? a.slab_box_k : ks;    // slab row stride (samples)
   const int kal = kmin & ~3;                           // 16-byte aligned segment start
-  if (use_tma) {
-    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\nfence.mbarrier_init.release.cluster;" ::"r"(b),
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; b++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[b])),
                    "r"(32)
                    : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&empty[b])),
+                   "r"(8)
+                   : "memory");
     }
-    __syncthreads();
-    if (warp == 0) {
-      // one 1-D bulk copy (TMA, UBLKCP) per line segment [kal, kal + box_k)
-      // (clipped to the record), lanes take lines
-      const float* src = (const float*)a.line_img + fbase;
-      const int seg = min(a.slab_box_k, S - kal);
-      unsigned bytes = 0;
-      for (int l = lane; l < nl && kmin >= 0; l += 32) bytes += (unsigned)seg * 4u;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-      for (int l = lane; l < nl && kmin >= 0; l += 32)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                (uint32_t)__cvta_generic_to_shared(slab + l * a.slab_box_k)),
-            "l"(src + (size_t)(l0 + l) * S + kal), "r"((unsigned)seg * 4u), "r"(b)
-            : "memory");
-    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (kmin >= 0 && nl > 0 && !use_tma) {
-    if (a.in_type == SUPRA_T_F32) {
-      const float* src = (const float*)a.line_img + fbase;
-      for (int l = warp; l < nl; l += 8)
-        for (int kk = lane; kk < ks; kk += 32)
-          cp_async4(slab + l * ks + kk, src + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
-    } else {
-      for (int l = warp; l < nl; l += 8)
-        for (int kk = lane; kk < ks; kk += 32)
-          slab[l * ks + kk] = load_y(a.line_img, a.in_type, fbase + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
-    }
-  }
-  if (threadIdx.x < rows) cp_async8(saz + threadIdx.x, a.az + z0 + threadIdx.x);
-  asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+  if (threadIdx.x < rows) saz[threadIdx.x] = a.az[z0 + threadIdx.x];
   const ScAxis ax = x < nx ? a.ax[x] : ScAxis{-1, 0.f};
-  __syncthreads();
-  if (use_tma) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W_%=;\n\t}" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&bar))
-        : "memory");
-  }
-  // depth lerp t[r][l]; rows without a valid k0 and the spare pair of
-  // columns [kScMaxLines, kScMaxLines+1] are zero, so the pixel loop below
-  // needs no predicates (invalid columns read the zero pair with fx = 0)
-  constexpr int TZS = kScMaxLines + 2;
-  if ((int)threadIdx.x < nl) {
-    const float* y = slab + threadIdx.x * kstride - (use_tma ? kal : kmin);
-    for (int r = 0; r < rows; r++) {
-      const ScAxis az = saz[r];
-      tz[r * TZS + threadIdx.x] = az.i0 >= 0 ? fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]) : 0.f;
-    }
-  }
-  if (threadIdx.x < 2 * kScRows) tz[(threadIdx.x >> 1) * TZS + kScMaxLines + (threadIdx.x & 1)] = 0.f;
-  __syncthreads();
-  if (x >= nx) return;
+  // lines this warp's columns touch: [wl0, wl0 + wnl) (slab-relative)
   const bool colok = ax.i0 >= 0;
-  const float* tcol = tz + (colok ? ax.i0 - l0 : kScMaxLines);
+  const unsigned wlo = __reduce_min_sync(0xffffffffu, colok ? (unsigned)(ax.i0 - l0) : 0xffffffffu);
+  const unsigned whi = __reduce_max_sync(0xffffffffu, colok ? (unsigned)(ax.i0 - l0 + 1) : 0u);
+  const int wl0 = wlo == 0xffffffffu ? 0 : (int)wlo;
+  const int wnl = wlo == 0xffffffffu ? 0 : (int)(whi - wlo + 1);  // <= kScWarpLines - 1 (checked at create)
+  float* tz = tzw[warp];
+  // zero pair for invalid columns, and per-column pointers
+  const float* tcol = tz + (colok ? ax.i0 - l0 - wl0 : kScWarpLines - 1);
   const float fx = colok ? ax.f : 0.f;
-  const size_t out0 = ((size_t)f * a.nz + z0) * nx + x;
-  if (U8OUT) {
-    uint8_t* o = (uint8_t*)a.img + out0;
-#pragma unroll 8
-    for (int r = 0; r < rows; r++, o += nx) {
-      const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
-      *o = (uint8_t)floorf(fmaf(255.f, fmaf(fx, t1 - t0, t0), 0.5f));
-    }
-  } else {
-    float* o = (float*)a.img + out0;
-#pragma unroll 8
-    for (int r = 0; r < rows; r++, o += nx) {
-      const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
-      *o = fmaf(fx, t1 - t0, t0);
-    }
+  for (int r = lane; r < kScRows; r += 32) {
+    tz[r * TZS + kScWarpLines - 1] = 0.f;
+    tz[r * TZS + kScWarpLines] = 0.f;
   }
-  if (a.mask && f == 0)
-    for (int r = 0; r < rows; r++) a.mask[(size_t)(z0 + r) * nx + x] = (colok && saz[r].i0 >= 0) ? 1 : 0;
+  __syncthreads();
+  auto wait = [](uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(bar)),
+        "r"(parity)
+        : "memory");
+  };
+  // one 1-D bulk copy (TMA, UBLKCP) per line segment [kal, kal + box_k)
+  // (clipped to the record), lanes of warp 0 take lines
+  auto issue = [&](int f, int b) {
+    const float* src = (const float*)a.line_img + (size_t)f * Lx * S;
+    const int seg = min(a.slab_box_k, S - kal);
+    const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&full[b]);
+    unsigned bytes = 0;
+    for (int l = lane; l < nl && kmin >= 0; l += 32) bytes += (unsigned)seg * 4u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+    for (int l = lane; l < nl && kmin >= 0; l += 32)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              (uint32_t)__cvta_generic_to_shared(slab[b] + l * a.slab_box_k)),
+          "l"(src + (size_t)(l0 + l) * S + kal), "r"((unsigned)seg * 4u), "r"(bb)
+          : "memory");
+  };
+  if (use_tma && warp == 0 && fbeg < fend) issue(fbeg, 0);
+  const ScAxis az = saz[lane < rows ? lane : 0];
+  for (int f = fbeg; f < fend; f++) {
+    const int it = f - fbeg, b = use_tma ? (it & 1) : 0;
+    if (use_tma) {
+      // refill the other buffer with the next frame once every warp has
+      // finished its depth lerp on it (previous iteration)
+      if (warp == 0 && f + 1 < fend) {
+        if (it >= 1) wait(&empty[b ^ 1], (unsigned)(((it - 1) >> 1) & 1));
+        issue(f + 1, b ^ 1);
+      }
+      wait(&full[b], (unsigned)((it >> 1) & 1));
+    } else {
+      if (it > 0) __syncthreads();  // every warp is done with slab[0]
+      if (kmin >= 0 && nl > 0) {
+        const size_t fbase = (size_t)f * Lx * S;
+        if (a.in_type == SUPRA_T_F32) {
+          const float* src = (const float*)a.line_img + fbase;
+          for (int l = warp; l < nl; l += 8)
+            for (int kk = lane; kk < ks; kk += 32)
+              cp_async4(slab[0] + l * ks + kk, src + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
+          asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+        } else {
+          for (int l = warp; l < nl; l += 8)
+            for (int kk = lane; kk < ks; kk += 32)
+              slab[0][l * ks + kk] =
+                  load_y(a.line_img, a.in_type, fbase + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
+        }
+      }
+      __syncthreads();
+    }
+    // depth lerp of this warp's lines: lane = output row; rows without a
+    // valid k0 are zero
+    for (int j = 0; j < wnl; j++) {
+      const float* y = slab[b] + (wl0 + j) * kstride - (use_tma ? kal : kmin);
+      if (lane < rows) tz[lane * TZS + j] = az.i0 >= 0 ? fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]) : 0.f;
+    }
+    __syncwarp();
+    if (use_tma && lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(&empty[b]))
+                   : "memory");
+    if (x < nx) {
+      const size_t out0 = ((size_t)f * a.nz + z0) * nx + x;
+      if (U8OUT) {
+        // u8 = floor(255 y + 1/2) (reading #20) by the magic-number floor
+        // (FADD.RM on the full-rate FP32 pipe; F2I is quarter rate): the
+        // low byte of the float bits of fl(255y + 1/2) + 1.5 2^23, rounded
+        // toward -inf, is the integer
+        uint8_t* o = (uint8_t*)a.img + out0;
+#pragma unroll 8
+        for (int r = 0; r < rows; r++, o += nx) {
+          const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
+          const float v = fmaf(255.f, fmaf(fx, t1 - t0, t0), 0.5f);
+          *o = (uint8_t)__float_as_uint(__fadd_rd(v, 12582912.0f));
+        }
+      } else {
+        float* o = (float*)a.img + out0;
+#pragma unroll 8
+        for (int r = 0; r < rows; r++, o += nx) {
+          const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
+          *o = fmaf(fx, t1 - t0, t0);
+        }
+      }
+      if (a.mask && f == 0)
+        for (int r = 0; r < rows; r++) a.mask[(size_t)(z0 + r) * nx + x] = (colok && saz[r].i0 >= 0) ? 1 : 0;
+    }
+    __syncwarp();  // this warp's tz is free for the next frame
+  }
 }
 
 // Linear 2D, direct (grids too coarse for the tiled kernel's slab): one
@@ -218,9 +259,15 @@ cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st) {
     sc_linear_direct_kernel<<<g2, 256, 0, st>>>(a);
     return cudaGetLastError();
   }
-  dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, a.F);
-  if (a.out_type == SUPRA_T_U8) sc_linear_tiled_kernel<true><<<grid, 256, 0, st>>>(a);
-  else sc_linear_tiled_kernel<false><<<grid, 256, 0, st>>>(a);
+  // frames per CTA: enough CTAs for ~4 waves of 148 SMs x 4 resident,
+  // the rest of the frames walked by each CTA with double-buffered staging
+  const long tiles = (long)((a.nx + 255) / 256) * ((a.nz + kScRows - 1) / kScRows);
+  const long want = 148L * 4 * 4;
+  int fpc = (int)std::max<long>(1, (tiles * a.F + want - 1) / want);
+  fpc = std::min(fpc, a.F);
+  dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, (a.F + fpc - 1) / fpc);
+  if (a.out_type == SUPRA_T_U8) sc_linear_tiled_kernel<true><<<grid, 256, 0, st>>>(a, fpc);
+  else sc_linear_tiled_kernel<false><<<grid, 256, 0, st>>>(a, fpc);
   return cudaGetLastError();
 }
 
