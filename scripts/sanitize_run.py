@@ -1,0 +1,45 @@
+"""Small invocations of every product kernel for compute-sanitizer (memcheck /
+racecheck / synccheck): single-frame warp-split DAS (Hann and Hamming, t0,
+nearest), batch DAS with row-cut maps and a PDL remainder launch, band
+bank + decimation, channel map, linear / sector / pyramid scan conversion,
+standalone envelope, line-range split.  Dev/validation aid."""
+import os
+import sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import torch  # noqa: E402
+from synth import configs  # noqa: E402
+from paper_1711_06127_b200 import SupraBF  # noqa: E402
+from gpu_util import raw_frames  # noqa: E402
+
+
+def run(w, F, lines=False):
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    rf, li, img, mask = bf.empty_rf(F), bf.empty_line_img(F), bf.empty_img(F), bf.empty_mask()
+    bf.beamform(raw, F, rf=rf, line_img=li)
+    bf.scanconvert(li, F, img, mask)
+    li2 = bf.empty_line_img(F)
+    bf.envelope_log(rf, F, li2)
+    if lines:
+        env = torch.zeros((1, w.L, w.S), dtype=torch.float32, device="cuda")
+        fm = torch.zeros((1,), dtype=torch.float32, device="cuda")
+        bf.beamform_lines(raw[:1], 1, 3, w.L // 2, env, fm)
+    torch.cuda.synchronize()
+    bf.close()
+    print("ok", w.name, F, flush=True)
+
+
+run(configs.c1(), 1, lines=True)
+run(configs.c1(window=configs.WIN_HAMMING, t0_s=1e-7), 1)
+run(configs.c1(interpolation=configs.INTERP_NEAREST, decimation=3,
+               bands=((5.5e6, 2.4e6, 0.5), (8.5e6, 2.4e6, 0.5))), 1)
+run(configs.c1(), 6)                                  # FB=4 + remainder 2 (PDL)
+run(configs.c2(), 3 if len(sys.argv) < 2 else int(sys.argv[1]))
+run(configs.table1(64, 2), 2)
+run(configs.c3(num_lines_x=16, line_origin_mm=configs.phased_lines(16, 60.0)[0],
+               line_direction=configs.phased_lines(16, 60.0)[1], num_events=16,
+               line_event=__import__("numpy").arange(16, dtype="int32"),
+               tx_origin_mm=__import__("numpy").zeros((16, 3)), S=1024), 2)
+print("all ok")
