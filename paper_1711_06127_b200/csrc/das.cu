@@ -143,13 +143,8 @@ __device__ __forceinline__ void tile_accumulate(const TapGeo& g, const unsigned 
   const uint32_t pa = smem_u32(st) + 2u * (uint32_t)idx;
 #pragma unroll
   for (int q = 0; q < FB / 2; q++) {
-#if defined(SUPRA_EXP_NO_X1)  // measurement only: wrong numerics
-    const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
-    const float2 x1 = make_float2(x0.y, x0.x);
-#else
     const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
     const float2 x1 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR + 2), lds_s16f(pa, 2 * (2 * q + 1) * FR + 2));
-#endif
     accp[q] = __ffma2_rn(make_float2(g.w0, g.w0), x0, accp[q]);
     accp[q] = __ffma2_rn(make_float2(g.w1, g.w1), x1, accp[q]);
   }
