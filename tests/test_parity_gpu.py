@@ -449,3 +449,23 @@ def test_c2_decimation_batch():
     assert rf_err(rf_g[1], rf_o) <= RF_TOL
     y_o, _ = oracle.log_compress(env_o, w.dynamic_range_db)
     assert np.max(np.abs(y_g[1].astype(int) - oracle.to_u8(y_o).astype(int))) <= 1
+
+
+# ------------------------- tensor-core FIR epilogue (16-frame batches, 65 taps)
+@pytest.mark.parametrize("over", [dict(), dict(reference_mode=configs.REF_FIXED, reference_value=800.0,
+                                               line_output_type=configs.T_U8),
+                                  dict(fir_taps=33)])            # 33 taps: the SIMT epilogue
+def test_c2_sixteen_frame_batch_epilogue(over):
+    w = configs.c2(**over)
+    F = 16
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    rf_g, y_g = run_gpu(bf, raw, F)
+    for f in (0, 5, 15):
+        rf_o, env_o = oracle_chain(w, raw[f].cpu().numpy())
+        assert rf_err(rf_g[f], rf_o) <= RF_TOL
+        y_o, _ = oracle.log_compress(env_o, w.dynamic_range_db, w.reference_mode, w.reference_value)
+        if w.line_output_type == configs.T_U8:
+            assert np.max(np.abs(y_g[f].astype(int) - oracle.to_u8(y_o).astype(int))) <= 1
+        else:
+            assert db_err(y_g[f], y_o) <= DB_TOL, f
