@@ -227,7 +227,7 @@ def main():
     import synth
     from synth import configs
     from paper_1711_06127_b200 import SupraBF
-    from paper_1711_06127_b200.dist import gather_bmode
+    from paper_1711_06127_b200.dist import OverlappedGather
     from paper_1711_06127_b200.pipeline import HostPipeline
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -253,19 +253,23 @@ def main():
     li = bf.empty_line_img(F)
     img = bf.empty_img(F)
     nx, ny, nz = w.out_dims
-    gather = None
-    if world > 1:
-        gather = [torch.empty_like(img) for _ in range(world)] if rank == 0 else None
+    # N > 1: the u8 B-mode batch of step i is gathered to rank 0 (NCCL) while
+    # step i + 1 beamforms (double-buffered images, stream-ordered waits)
+    gat = OverlappedGather(img, dst=0)
     stream = torch.cuda.current_stream(dev)
+    nstep = [0]
 
     def step():
+        i = nstep[0]
+        nstep[0] += 1
+        out = gat.buffer(i)
         bf.beamform(raw, F, line_img=li)
-        bf.scanconvert(li, F, img)
-        if world > 1:
-            gather_bmode(img, dst=0, out=gather)
+        bf.scanconvert(li, F, out)
+        gat.submit(i)
 
     for _ in range(max(3, args.warmup)):
         step()
+    gat.drain()
     torch.cuda.synchronize()
 
     K = args.steps
@@ -288,6 +292,7 @@ def main():
     for i in range(K):
         bf.set_das_events(*das_ev[i])
         step()
+    gat.drain()          # the last gathers belong to the timed steps
     stop.record(stream)
     torch.cuda.synchronize()
     bf.set_das_events(None, None)

@@ -35,6 +35,47 @@ def gather_bmode(img: torch.Tensor, dst: int = 0,
     return out if rank == dst else None
 
 
+class OverlappedGather:
+    """Double-buffered asynchronous gather of B-mode batches to ``dst`` so the
+    transfer of step i overlaps the beamforming of step i + 1 (SURVEY 8(e):
+    rank-0 ingress, not compute, bounds the frame-sharded stream beyond a few
+    GPUs).  ``buffer(i)`` is the image batch step i must write; before it is
+    handed out again (step i + 2) the stream waits for its previous gather.
+    ``received(i)`` on ``dst`` is the list of every rank's batch of step i
+    once ``drain()`` (or the wait inside ``buffer(i + 2)``) has run."""
+
+    def __init__(self, like: torch.Tensor, dst: int = 0, nbuf: int = 2):
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.dst = dst
+        self.bufs = [like if i == 0 else torch.empty_like(like) for i in range(nbuf)]
+        self.recv = [[torch.empty_like(like) for _ in range(self.world)] if self.rank == dst else None
+                     for _ in range(nbuf)]
+        self.work = [None] * nbuf
+
+    def buffer(self, i: int) -> torch.Tensor:
+        b = i % len(self.bufs)
+        if self.work[b] is not None:
+            self.work[b].wait()        # stream-ordered: the current stream waits, the host does not
+            self.work[b] = None
+        return self.bufs[b]
+
+    def submit(self, i: int):
+        if self.world == 1:
+            return
+        b = i % len(self.bufs)
+        self.work[b] = dist.gather(self.bufs[b], gather_list=self.recv[b], dst=self.dst, async_op=True)
+
+    def drain(self):
+        for b, w in enumerate(self.work):
+            if w is not None:
+                w.wait()
+                self.work[b] = None
+
+    def received(self, i: int):
+        return self.recv[i % len(self.bufs)] if self.world > 1 else [self.bufs[i % len(self.bufs)]]
+
+
 def frame_max_allreduce(frame_max: torch.Tensor) -> torch.Tensor:
     """All-reduce(max) of per-frame envelope maxima -- the exchange needed
     when one volume's scanline blocks are split across ranks (the frame-max

@@ -148,3 +148,48 @@ def test_sharded_volume_gloo_world2(L, align):
         y, m = res[r]
         assert m == float(L * S)                       # the global frame max on every rank
         assert abs(y[0] - expect).max() < 1e-6         # every rank holds the whole line image
+
+
+def _overlap_worker(rank, world, port, q):
+    from paper_1711_06127_b200.dist import OverlappedGather
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        like = torch.zeros((2, 1, 4), dtype=torch.uint8)
+        g = OverlappedGather(like, dst=0)
+        seen = []
+        for i in range(5):
+            buf = g.buffer(i)
+            if i >= 2 and rank == 0:      # the gather of step i - 2 has completed
+                seen.append((i - 2, [t.tolist() for t in g.received(i - 2)]))
+            buf.fill_(10 * i + rank)       # "beamform" step i into the handed-out buffer
+            g.submit(i)
+        g.drain()
+        if rank == 0:
+            for i in (3, 4):
+                seen.append((i, [t.tolist() for t in g.received(i)]))
+        q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_gather_double_buffer_gloo_world2():
+    """The double-buffered asynchronous B-mode gather of bench.py: every step's
+    batches arrive at rank 0 in rank order, and a buffer is not handed out
+    again before its previous gather completed."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    steps = dict(res[0])
+    assert sorted(steps) == [0, 1, 2, 3, 4]
+    for i, got in steps.items():
+        assert got == [torch.full((2, 1, 4), 10 * i + r, dtype=torch.uint8).tolist() for r in range(world)]
