@@ -13,9 +13,10 @@ OUT = os.path.join(HERE, "libsupra_bf.so")
 BUILD = os.path.join(HERE, "_build")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["das.cu", "das_warp.cu", "epilogue.cu", "scanconv.cu"]
+CU = (["das.cu"] + [f"das_inst{i}.cu" for i in range(6)] + ["das_warp.cu"] +
+      [f"das_warp_inst{i}.cu" for i in range(3)] + ["epilogue.cu", "scanconv.cu"])
 CPP = ["host.cpp"]
-HDRS = ["internal.h", "epilogue.cuh", "das_common.cuh"]
+HDRS = ["internal.h", "epilogue.cuh", "das_common.cuh", "das_kernel.cuh", "das_warp_kernel.cuh"]
 
 
 def _run(cmd, verbose):
@@ -44,16 +45,22 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, var
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     hdr_deps = [os.path.join(CSRC, h) for h in HDRS] + [os.path.join(ROOT, "include", "supra_bf.h")]
     objs = []
+    cmds = []
     for f in CU:
         src = os.path.join(CSRC, f)
         obj = os.path.join(BUILD, f + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdr_deps):
             cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, *dflags, "-O3", "-lineinfo", "-std=c++17",
-                   "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", *inc, "-c", src, "-o", obj]
+                   "--expt-relaxed-constexpr", "-Xfatbin=-compress-all", "-Xcompiler", "-fPIC", *inc, "-c", src, "-o", obj]
             if ptxas_v:
                 cmd.insert(1, "-Xptxas=-v")
-            _run(cmd, verbose)
+            cmds.append(cmd)
+    # translation units compile in parallel (the DAS variants are split over
+    # das_inst*.cu / das_warp_inst*.cu for this)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda c: _run(c, verbose), cmds))
     for f in CPP:
         src = os.path.join(CSRC, f)
         obj = os.path.join(BUILD, f + ".o")

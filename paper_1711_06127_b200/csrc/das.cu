@@ -1,483 +1,39 @@
-// das.cu -- sm_100a delay-and-sum receive beamforming with the fused
-// IQ-envelope / log-compression epilogue (
-// S:133).
-//
-// One CTA = one scanline x FB frames (256 threads, 2 CTAs per SM).  Depth is
-// processed in passes of PL = 256 NT samples; in a pass every thread keeps
-// the RF of its NT output samples k = k0 + kt + 256 m for all FB frames in
-// registers (FB x NT = 64 accumulators, packed f32x2).  Per pass the loop
-// runs over the line's receive-aperture entries (channels sorted by
-// aperture entry depth k_enter in binary64, reading #6) that are members
-// somewhere in the pass:
-//   * per entry ONE 5-D TMA (cp.async.bulk.tensor -> SASS UTMALDG) fetches
-//     the entry's referenced trace window for the pass, for all FB frames,
-//     into a shared-memory ring; samples < 0 or >= S come back as zeros
-//     (the TMA out-of-bounds fill = the zero padding of reading #10).  The
-//     last warp to release a ring slot refills it -- no producer warp.
-//   * per entry and output tile: the closed-form split delay tau = k + delta,
-//     delta = |q + h d| - h (h = k/2 in sample units) with one MUFU.RSQ +
-//     Newton correction (reading #30), magic-number floor, Hann weight
-//     (MUFU.COS), then per frame pair two sign-extending LDS.S16 + I2FP and
-//     the interpolating accumulation in FFMA2: the geometry is amortised
-//     over the FB frames.
-// After a pass RF = sum / N (N from a binary64-derived count table) goes to
-// a padded shared-memory line buffer (aliasing the drained ring) and the
-// 65-tap complex FIR runs over the outputs whose taps are complete, as a
-// sliding window (4 outputs x 4 frames per thread, taps in the constant
-// bank); the last 2P RF samples carry over to the next pass.  |.|, then
-// 20 log10 against a fixed reference, or env + per-frame max for the
-// frame-max reference (finalised by finalize_kernel).
-#include "internal.h"
-
+// das.cu -- launch-shape selection and dispatch of the DAS batch kernel
+// (das_kernel.cuh); the kernel variants are instantiated in das_inst*.cu.
 #include <cstdio>
 #include <cstdlib>
 
-#include "das_common.cuh"
+#include "das_kernel.cuh"
 
 namespace supra {
 
-namespace {
-
-
-struct SmemLayout {
-  int16_t* stage;   // [NS][stage_bytes]
-  float4* line;     // FIR line buffer, aliases the stage ring between passes
-  float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
-  int2* wse;        // [nent] {window start ws, channel | rcut << 20}
-  float4* carry;    // [ngroups][2P] RF tail of the previous pass
-  uint64_t* full;   // [kMaxStages]
-  unsigned* rel;    // [kMaxStages] warps done with the slot (last one refills it)
-  unsigned* smax;   // [16] per-frame envelope max (float bits)
-};
-
-// Bytes of everything except the ring; ring stages fill the rest of the
-// per-CTA budget (2 CTAs per SM), between 3 and kMaxStages.
-__host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P) {
-  return align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
-         align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1)) + align128(sizeof(uint64_t) * kMaxStages) +
-         align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16);
-}
-// CTAs per SM: 3 for short passes (NT = 2: 32 accumulators, <= 85
-// registers), else 2; the per-CTA shared-memory budget follows.
-__host__ __device__ constexpr int das_ctas_per_sm(int NT) { return NT == 2 ? 3 : 2; }
-__host__ __device__ constexpr size_t das_smem_budget(int NT) { return NT == 2 ? 75 * 1024 : 113 * 1024; }
-
-__host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P) {
-  const size_t fixed = fixed_bytes(FB, nent_max, P);
-  const size_t sb = stage_bytes(FB, das_rows_nt(NT));
-  const size_t budget = das_smem_budget(NT);
-  const long n = fixed >= budget ? 0 : (long)((budget - fixed) / sb);
-  return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : (int)n);
-}
-
-__host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int P, size_t* off) {
-  const size_t ring = (size_t)das_stages(FB, NT, nent_max, P) * stage_bytes(FB, das_rows_nt(NT));
-  const size_t fb = align128((size_t)fir_groups(FB) * fir_span(NT * kTileK, P) * 16);
-  size_t o = 0;
-  off[0] = o; o = align128(o + (ring > fb ? ring : fb));
-  off[1] = o; o = align128(o + sizeof(float4) * nent_max);
-  off[2] = o; o = align128(o + sizeof(int2) * nent_max);
-  off[3] = o; o = align128(o + sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
-  off[4] = o; o = align128(o + sizeof(uint64_t) * kMaxStages);
-  off[5] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
-  off[6] = o; o = align128(o + sizeof(unsigned) * 16);
-  return o;
-}
-
-__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT, int nent_max, int P) {
-  size_t off[7];
-  layout_bytes(FB, NT, nent_max, P, off);
-  SmemLayout L;
-  L.stage = (int16_t*)(base + off[0]);
-  L.line = (float4*)(base + off[0]);
-  L.rec = (float4*)(base + off[1]);
-  L.wse = (int2*)(base + off[2]);
-  L.carry = (float4*)(base + off[3]);
-  L.full = (uint64_t*)(base + off[4]);
-  L.rel = (unsigned*)(base + off[5]);
-  L.smax = (unsigned*)(base + off[6]);
-  return L;
-}
-
-}  // namespace
-
-// Accumulators of one thread: NT output samples x FB frames.
-// FB = 1: tiles (2i, 2i+1) packed in s2[i]; FB >= 2: frame pairs in p[m][q].
-template <int FB, int NT>
-struct Acc {
-  float2 s2[FB == 1 ? NT / 2 : 1];
-  float2 p[FB >= 2 ? NT : 1][FB >= 2 ? FB / 2 : 1];
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int m = 0; m < NT; m++) {
-      if constexpr (FB == 1) {
-        if (m % 2 == 0) s2[m / 2] = make_float2(0.f, 0.f);
-      } else {
-#pragma unroll
-        for (int q = 0; q < FB / 2; q++) p[m][q] = make_float2(0.f, 0.f);
-      }
-    }
-  }
-  __device__ __forceinline__ float s(int m) const { return (m & 1) ? s2[m / 2].y : s2[m / 2].x; }
-};
-
-// Per-tile tap geometry: index of x[i0] in the staged window and the two
-// interpolation weights.
-struct TapGeo {
-  int idx;
-  float w0, w1;
-};
-
-// Specialisation granularity of the first active tile (code size).
-__host__ __device__ constexpr int tile_gran(int NT) { return NT <= 8 ? 1 : 2; }
-
-// Accumulate one tile's tap for all FB frames (per frame pair: 4 sign-
-// extending LDS.S16 + I2FP, 2 FFMA2; frames at immediate offsets).
-template <int FB, int NT>
-__device__ __forceinline__ void tile_accumulate(const TapGeo& g, const unsigned short* st, float2* accp) {
-  constexpr int FR = (NT * 8 + 2) * kRowSamples;
-  int idx = g.idx;
-  // opaque copy: keeps one materialised index so the FB loads below use
-  // immediate offsets instead of one address add each
-  asm("mov.b32 %0, %0;" : "+r"(idx));
-  const uint32_t pa = smem_u32(st) + 2u * (uint32_t)idx;
-#pragma unroll
-  for (int q = 0; q < FB / 2; q++) {
-    const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
-    const float2 x1 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR + 2), lds_s16f(pa, 2 * (2 * q + 1) * FR + 2));
-    accp[q] = __ffma2_rn(make_float2(g.w0, g.w0), x0, accp[q]);
-    accp[q] = __ffma2_rn(make_float2(g.w1, g.w1), x1, accp[q]);
-  }
-}
-
-// Geometry of tile m alone (scalar).  The warp's first member tile is >= M0
-// and k_enter < k0 + (M0 + gran) * 256, so only the first gran tiles can
-// hold non-members (their weight and index are zeroed).  Outputs k >= S are
-// computed but never stored; their taps stay inside the window.
-template <int NT, int M0, bool T0>
-__device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4& r, int kenter, int wsm,
-                                           int kt, int k0, float kt0f) {
-  const int k = k0 + m * kTileK + kt;
-  const bool mem = !(m < M0 + tile_gran(NT)) || k >= kenter;
-  const float kf = kt0f + (float)(m * kTileK);
-  const float h = 0.5f * kf;
-  const float h2 = (m == 0 && k == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
-  float delta = split_delay(r.x, r.y, h, h2);
-  if (T0) delta += a.t0fs;
-  const float tf = __fadd_rd(delta, kFloorMagic);
-  const int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - k0 - kt)
-  const float fr = (delta - (tf - kFloorMagic)) * a.fr_scale;
-  float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
-  w = mem ? w : 0.f;
-  // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
-  const float w1 = w * fr;
-  return TapGeo{mem ? idx : 0, w - w1, w1};
-}
-
-// Geometry of tiles m, m+1 together in packed f32x2 (FFMA2 / FADD2.RM /
-// FMUL2: about 40 % fewer issued instructions than two scalar tiles; the
-// per-lane arithmetic is the same, so results are identical).
-template <int NT, int M0, bool T0>
-__device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4& r, int kenter, int wsm, int kt,
-                                          int k0, float kt0f, TapGeo& g0, TapGeo& g1) {
-  const int ka = k0 + m * kTileK + kt;
-  const bool mem0 = !(m < M0 + tile_gran(NT)) || ka >= kenter;
-  const bool mem1 = !(m + 1 < M0 + tile_gran(NT)) || ka + kTileK >= kenter;
-  const float2 kf = make_float2(kt0f + (float)(m * kTileK), kt0f + (float)((m + 1) * kTileK));
-  const float2 h = __fmul2_rn(kf, make_float2(0.5f, 0.5f));
-  float2 h2 = __fmul2_rn(h, h);
-  if (m == 0 && ka == 0) h2.x = 1e-20f;
-  float2 delta = split_delay2(r.x, r.y, h, h2);
-  if (T0) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));
-  const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
-  const int idx0 = __float_as_int(tf.x) - wsm + m * kTileK;
-  const int idx1 = __float_as_int(tf.y) - wsm + (m + 1) * kTileK;
-  const float2 fr = __fmul2_rn(sub2(delta, sub2(tf, make_float2(kFloorMagic, kFloorMagic))),
-                               make_float2(a.fr_scale, a.fr_scale));
-  const float2 u = __fmul2_rn(make_float2(r.z, r.z),
-                              make_float2(rcp_ftz(fmaxf(kf.x, 1.f)), rcp_ftz(fmaxf(kf.y, 1.f))));
-  float2 w = __ffma2_rn(make_float2(__cosf(u.x), __cosf(u.y)), make_float2(a.win_b, a.win_b),
-                        make_float2(a.win_a, a.win_a));
-  w.x = mem0 ? w.x : 0.f;
-  w.y = mem1 ? w.y : 0.f;
-  const float2 w1 = __fmul2_rn(w, fr);
-  const float2 w0 = sub2(w, w1);
-  g0 = TapGeo{mem0 ? idx0 : 0, w0.x, w1.x};
-  g1 = TapGeo{mem1 ? idx1 : 0, w0.y, w1.y};
-}
-
-// One aperture entry, output tiles M0 .. NT-1 of the pass (straight-line):
-// an odd first tile alone, then tile pairs (2i, 2i+1) in packed geometry.
-// kt0f = (float)(k0 + kt): the thread's first output sample in the pass.
-template <int FB, int NT, int M0, bool T0>
-__device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, int kenter, int wsm,
-                                            const unsigned short* st, int kt, int k0, float kt0f,
-                                            Acc<FB, NT>& acc) {
-  if constexpr (M0 & 1) {
-    const TapGeo g = tile_geo<NT, M0, T0>(M0, a, r, kenter, wsm, kt, k0, kt0f);
-    if constexpr (FB == 1) {
-      const uint32_t pa = smem_u32(st) + 2u * (uint32_t)g.idx;
-      float& s1 = acc.s2[M0 / 2].y;
-      s1 = fmaf(g.w0, lds_s16f(pa, 0), s1);
-      s1 = fmaf(g.w1, lds_s16f(pa, 2), s1);
-    } else {
-      tile_accumulate<FB, NT>(g, st, acc.p[M0]);
-    }
-  }
-#pragma unroll
-  for (int m = (M0 + 1) & ~1; m < NT; m += 2) {
-    TapGeo g0, g1;
-    tile_geo2<NT, M0, T0>(m, a, r, kenter, wsm, kt, k0, kt0f, g0, g1);
-    if constexpr (FB == 1) {
-      const uint32_t p0 = smem_u32(st) + 2u * (uint32_t)g0.idx, p1 = smem_u32(st) + 2u * (uint32_t)g1.idx;
-      const float2 x0 = make_float2(lds_s16f(p0, 0), lds_s16f(p1, 0));
-      const float2 x1 = make_float2(lds_s16f(p0, 2), lds_s16f(p1, 2));
-      acc.s2[m / 2] = __ffma2_rn(make_float2(g0.w0, g1.w0), x0, acc.s2[m / 2]);
-      acc.s2[m / 2] = __ffma2_rn(make_float2(g0.w1, g1.w1), x1, acc.s2[m / 2]);
-    } else {
-      tile_accumulate<FB, NT>(g0, st, acc.p[m]);
-      tile_accumulate<FB, NT>(g1, st, acc.p[m + 1]);
-    }
-  }
-}
-
-template <int FB, int NT, bool T0, int G = 0>
-__device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const float4& r, int kenter, int wsm,
-                                               const unsigned short* st, int kt, int k0, float kt0f,
-                                               Acc<FB, NT>& acc) {
-  constexpr int M0 = G * tile_gran(NT);
-  if constexpr (M0 < NT) {
-    if (g == G) entry_tiles<FB, NT, M0, T0>(a, r, kenter, wsm, st, kt, k0, kt0f, acc);
-    else dispatch_tiles<FB, NT, T0, G + 1>(g, a, r, kenter, wsm, st, kt, k0, kt0f, acc);
-  }
-}
-
-template <int FB, int NT, bool T0>
-__global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                          const DasArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int PL = NT * kTileK;                 // samples per pass
-  constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
-  const int S = a.S;
-  const int P = (a.fir_taps - 1) / 2;
-  const size_t SB = stage_bytes(FB, NT * 8 + 2);
-  SmemLayout sm = carve(smem_raw, FB, NT, a.entries_per_group, P);
-  const int line = a.line0 + blockIdx.x;
-  const int fm = blockIdx.y * FB;   // first frame of the CTA in the tensor map
-  const int f0 = a.fbase + fm;      // ... and in the call
-  if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int g = a.line_group[line];
-  const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
-  const int nent = a.nentries[g];
-  const int lane = threadIdx.x & 31;
-  const int ev = a.line_event[line];
-  const float4 dir = a.line_dir[line];
-  const int NS = das_stages(FB, NT, a.entries_per_group, P);
-  const int ng = fir_groups(FB);
-  const int span = fir_span(PL, P);
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; i++) {
-      mbar_init(&sm.full[i], 1);
-      sm.rel[i] = 0u;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-  }
-  if (a.raw_maps && (int)threadIdx.x < S / kRowSamples)
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.raw_maps + threadIdx.x))
-                 : "memory");
-  if (threadIdx.x < 16) sm.smax[threadIdx.x] = 0u;
-
-  const int kt = threadIdx.x;
-  const int kwarp_last = (kt | 31);
-  float bmax[4] = {0.f, 0.f, 0.f, 0.f};
-  int curg = -1;
-  int buf = 0;           // ring slot of the next entry (continues across passes)
-  unsigned phase = 0;    // its mbarrier parity
-  auto flush_max = [&]() {
-    if (curg >= 0 && !a.ref_fixed)
-      for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
-  };
-
-  for (int k0 = 0; k0 < S; k0 += PL) {
-    const int kend = min(S, k0 + PL);
-    // entries with a member sample in the pass: the k_enter-sorted prefix
-    // with k_enter < kend
-    int np = 0;
-    for (int i0 = 0; i0 < nent; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      np += __syncthreads_count(i < nent && ents[i].kenter < kend);
-    }
-    // Entry records of the pass, in device order: alternate the long-trace
-    // (early k_enter) and short-trace ends of the prefix so consecutive
-    // ring entries carry similar work.  Window [ws, ws + rows*32),
-    // rows = PL/32 + 2, ws <= floor(tau(kb)) - 2 and 32-aligned, kb =
-    // max(k_enter, k0): d tau/dk in [0, 1] keeps i0(k) + 1 inside the
-    // window for every member k of the pass; reads outside the record come
-    // back as TMA zeros.  (The sum order is fixed per configuration: results
-    // are deterministic and identical across frames and batch sizes.)
-    for (int i = threadIdx.x; i < np; i += blockDim.x) {
-      const DasEntry e = ents[(i & 1) ? np - 1 - i / 2 : i / 2];
-      const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
-      const float Ah = 0.5f * e.A;
-      const int kb = max(e.kenter, k0);
-      const float hb = 0.5f * (float)kb;
-      const float tb = (float)kb + split_delay(Ah, B, hb, kb > 0 ? hb * hb : 1e-20f) + a.t0fs;
-      const int ws = ((int)floorf(tb) - 2) & ~(kRowSamples - 1);
-      // exclusive end row of the pass's referenced samples: i0 + 1 <=
-      // floor(tau(kend - 1)) + 1 for every member k < kend (+1 margin)
-      const int kl = kend - 1;
-      const float hl = 0.5f * (float)kl;
-      const float tl = (float)kl + split_delay(Ah, B, hl, kl > 0 ? hl * hl : 1e-20f) + a.t0fs;
-      const int rcut = max(1, min(S / kRowSamples, ((int)floorf(tl) + 3 + kRowSamples - 1) / kRowSamples));
-      sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(e.kenter));
-      sm.wse[i] = make_int2(ws, e.elem | (rcut << 20));
-    }
-    __syncthreads();  // records visible; the previous pass is done with the line buffer
-
-    // TMA of entry jj's window (all FB frames) into ring slot `buf`.
-    auto produce = [&](int jj, int buf) {
-      const int2 we = sm.wse[jj];
-      // rows at or past rcut are out of bounds in raw_maps[rcut - 1]: zero
-      // fill, no DRAM read (the box size, and so the tx count, is fixed)
-      const CUtensorMap* m = a.raw_maps ? a.raw_maps + ((we.y >> 20) - 1) : &tmap;
-      mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
-      tma_load_5d((unsigned char*)sm.stage + buf * SB, m, 0, we.x / kRowSamples, we.y & 0xFFFFF, ev, fm,
-                  &sm.full[buf]);
-    };
-    if (threadIdx.x == 0 && a.debug_skip != 2) {
-      // the ring was last written through the generic proxy (line buffer)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      for (int jj = 0, b = buf; jj < NS && jj < np; jj++, b = (b + 1 == NS ? 0 : b + 1)) produce(jj, b);
-    }
-
-    Acc<FB, NT> acc;
-    acc.zero();
-    const float kt0f = (float)(k0 + kt);
-    for (int j = 0; j < np; j++) {
-      if (a.debug_skip != 2) mbar_wait(&sm.full[buf], phase);
-      const float4 r = sm.rec[j];
-      const int kenter = __float_as_int(r.w);
-      const int wsm = sm.wse[j].x + kFloorMagicBits - k0 - kt;
-      const unsigned short* st = (const unsigned short*)((const unsigned char*)sm.stage + buf * SB);
-      // first tile of the pass in which this WARP has a member sample
-      // (warp-uniform): straight-line code from there (the chains of
-      // consecutive tiles interleave); tiles where all 32 of the warp's k
-      // are < k_enter are skipped.
-      int m0 = kenter - k0 - kwarp_last;
-      m0 = m0 <= 0 ? 0 : (m0 + kTileK - 1) / kTileK;
-      if (a.debug_skip != 1 && m0 < NT)
-        dispatch_tiles<FB, NT, T0>(m0 / tile_gran(NT), a, r, kenter, wsm, st, kt, k0, kt0f, acc);
-      // release the slot; the last warp to release it refills it (no warp
-      // ever waits for another to issue a copy)
-      __syncwarp();
-      if (lane == 0) {
-        const unsigned prev = atom_add_acqrel(&sm.rel[buf], 1u);
-        if (prev == (blockDim.x / 32) - 1) {
-          sm.rel[buf] = 0u;
-          if (j + NS < np && a.debug_skip != 2) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            produce(j + NS, buf);
-          }
-        }
-      }
-      if (++buf == NS) {
-        buf = 0;
-        phase ^= 1u;
-      }
-    }
-    __syncthreads();  // every warp is done with the ring: it becomes the line buffer
-
-    // ---- RF = sum / N (reading #7; 0 when N = 0) ----
-    const uint16_t* ncount = a.ncount + (size_t)g * S;
-    const int kbase = k0 - 2 * P;  // line buffer position b = k - kbase
-#pragma unroll
-    for (int m = 0; m < NT; m++) {
-      const int k = k0 + m * kTileK + kt;
-      float v[FB];
-      if (k < S) {
-        const int n = (int)ncount[k];
-        const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
-        if constexpr (FB == 1) {
-          v[0] = acc.s(m) * inv;
-        } else {
-#pragma unroll
-          for (int q = 0; q < FB / 2; q++) {
-            v[2 * q] = acc.p[m][q].x * inv;
-            v[2 * q + 1] = acc.p[m][q].y * inv;
-          }
-        }
-        if (a.rf) {
-#pragma unroll
-          for (int b = 0; b < FB; b++)
-            if (f0 + b < a.F) a.rf[((size_t)(f0 + b) * a.L + line) * S + k] = v[b];
-        }
-      } else {
-#pragma unroll
-        for (int b = 0; b < FB; b++) v[b] = 0.f;  // zero padding past the record
-      }
-      if (a.do_epilogue) {
-        const int pk = fir_pad(k - kbase);
-#pragma unroll
-        for (int q4 = 0; q4 < (FB + 3) / 4; q4++) {
-          float4 x;
-          x.x = v[4 * q4];
-          x.y = (4 * q4 + 1 < FB) ? v[(4 * q4 + 1) % FB] : 0.f;
-          x.z = (4 * q4 + 2 < FB) ? v[(4 * q4 + 2) % FB] : 0.f;
-          x.w = (4 * q4 + 3 < FB) ? v[(4 * q4 + 3) % FB] : 0.f;
-          sm.line[(size_t)q4 * span + pk] = x;
-        }
-      }
-    }
-    if (!a.do_epilogue) continue;
-    // carried RF tail (or zeros before k = 0) and zeros after the pass
-    const int tail = P + 4;
-    for (int i = threadIdx.x; i < ng * (2 * P + tail); i += blockDim.x) {
-      const int q4 = i / (2 * P + tail), r = i - q4 * (2 * P + tail);
-      if (r < 2 * P)
-        sm.line[(size_t)q4 * span + fir_pad(r)] =
-            k0 == 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : sm.carry[q4 * 2 * P + r];
-      else
-        sm.line[(size_t)q4 * span + fir_pad(PL + r)] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    __syncthreads();
-    // ---- epilogue: outputs whose taps are complete in this pass ----
-    const int o_begin = k0 == 0 ? 0 : k0 - P;
-    const int o_end = kend == S ? S : k0 + PL - P;
-    const int nblk = (o_end - o_begin + 3) / 4;
-    for (int it = threadIdx.x; it < ng * nblk; it += blockDim.x) {
-      const int q4 = it / nblk, blk = it - q4 * nblk;
-      if (q4 != curg) {
-        flush_max();
-        curg = q4;
-        bmax[0] = bmax[1] = bmax[2] = bmax[3] = 0.f;
-      }
-      fir_block<FB>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, line, f0 + 4 * q4, bmax);
-    }
-    // RF tail k in [k0 + PL - 2P, k0 + PL) for the next pass's first outputs
-    if (kend < S)
-      for (int i = threadIdx.x; i < ng * 2 * P; i += blockDim.x) {
-        const int q4 = i / (2 * P), r = i - q4 * 2 * P;
-        sm.carry[i] = sm.line[(size_t)q4 * span + fir_pad(PL + r)];
-      }
-    // (the __syncthreads at the top of the next pass orders these reads
-    // before the ring is refilled)
-  }
-  if (a.do_epilogue && !a.ref_fixed) {
-    flush_max();
-    __syncthreads();
-    if (threadIdx.x < FB && f0 + (int)threadIdx.x < a.F)
-      atomicMax(&a.frame_max[f0 + threadIdx.x], sm.smax[threadIdx.x]);
-  }
-  // secondary launch of a split call: complete only after the primary grid
-  // (so work queued behind this kernel also sees the primary's results)
-  if (a.pdl_wait_end) asm volatile("griddepcontrol.wait;" ::: "memory");
-}
+extern template cudaError_t launch_k<16, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<16, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<8, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<8, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<8, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<8, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<4, 16, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<4, 16, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<4, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<4, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<4, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<4, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<2, 16, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<2, 16, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<2, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<2, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<2, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<2, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<1, 16, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<1, 16, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<1, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<1, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<1, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<1, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
 
 size_t das_smem_bytes(int FB, int NT, int nent_max, int fir_taps) {
-  size_t off[7];
-  return layout_bytes(FB, NT, nent_max, (fir_taps - 1) / 2, off);
+  return das_smem_bytes_impl(FB, NT, nent_max, fir_taps);
 }
 
 // (frames per CTA, tiles per pass): the first feasible candidate -- FB x NT
@@ -494,7 +50,7 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps) {
   if (const char* ev = std::getenv("SUPRA_BF_SHAPE")) std::sscanf(ev, "%dx%d", &ofb, &ont);
   for (int ci = -1; ci < (int)(sizeof cand / sizeof cand[0]); ci++) {
     const int fb = ci < 0 ? ofb : cand[ci][0], nt = ci < 0 ? ont : cand[ci][1];
-    if (ci < 0 && !((fb == 16 && (nt == 2 || nt == 4)) || (fb == 8 && (nt == 2 || nt == 4 || nt == 8)))) continue;
+    if (ci < 0 && !((fb == 16 && nt == 4) || (fb == 8 && (nt == 4 || nt == 8)))) continue;
     if (fb > fb_max || (fb > F && fb > 1) || nt > ntmax) continue;
     const size_t fixed = fixed_bytes(fb, nent_max, P);
     const size_t ring = 3 * stage_bytes(fb, das_rows_nt(nt));
@@ -505,33 +61,12 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps) {
   return DasShape{1, 4};
 }
 
-template <int FB, int NT, bool T0>
-static cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
-  const size_t smem = das_smem_bytes(FB, NT, a.entries_per_group, a.fir_taps);
-  auto kern = das_fused_kernel<FB, NT, T0>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.nlines, (a.Fmap + FB - 1) / FB);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = a.pdl_wait_end ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, tm, a);
-}
-
 template <bool T0>
 static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, DasShape sh, cudaStream_t st) {
   const int nt = sh.nt;
   switch (sh.fb) {
-    case 16: return nt == 2 ? launch_k<16, 2, T0>(tm, a, st) : launch_k<16, 4, T0>(tm, a, st);
-    case 8:
-      return nt == 2 ? launch_k<8, 2, T0>(tm, a, st)
-                     : (nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st));
+    case 16: return launch_k<16, 4, T0>(tm, a, st);
+    case 8: return nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st);
     case 4:
       return nt == 4 ? launch_k<4, 4, T0>(tm, a, st)
                      : (nt == 8 ? launch_k<4, 8, T0>(tm, a, st) : launch_k<4, 16, T0>(tm, a, st));
