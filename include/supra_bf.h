@@ -247,6 +247,22 @@ supra_status supra_bf_scanconvert(supra_bf_t h, const void *line_img, int32_t fr
                                   uint8_t *mask, void *stream);
 
 /*
+ * supra_bf_beamform_bmode -- the whole hot path in one call, raw channel data
+ * to B-mode image, without materialising the line image: DAS + IQ envelope
+ * into the handle's f32 line-domain scratch, then scan conversion that
+ * log-compresses each interpolation corner on load (frame-max reference:
+ * against the frame's envelope maximum; fixed reference: the
+ * epilogue already wrote y).  The image is bitwise the one of
+ * supra_bf_beamform(line_img = f32) + supra_bf_scanconvert; it saves the
+ * finalisation pass over the line image.
+ *   raw  : as supra_bf_beamform;  img, mask: as supra_bf_scanconvert.
+ * Errors: SUPRA_E_STRUCT on NULL / misaligned raw / frames out of range /
+ * pointers that are not device memory of cfg.device.
+ */
+supra_status supra_bf_beamform_bmode(supra_bf_t h, const void *raw, int32_t frames, void *img,
+                                     uint8_t *mask, void *stream);
+
+/*
  * supra_bf_destroy -- synchronise the device and free the handle's tables and
  * scratch.  NULL is a no-op.
  */

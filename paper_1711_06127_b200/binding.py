@@ -30,7 +30,8 @@ SC_LINEAR_2D, SC_SECTOR_2D, SC_PYRAMID_3D = 0, 1, 2
 
 EXPORTS = ("supra_bf_create", "supra_bf_beamform", "supra_bf_envelope_log", "supra_bf_scanconvert",
            "supra_bf_destroy", "supra_bf_last_error", "supra_bf_sc_indices", "supra_bf_info",
-           "supra_bf_set_das_events", "supra_bf_beamform_lines", "supra_bf_log_compress")
+           "supra_bf_set_das_events", "supra_bf_beamform_lines", "supra_bf_log_compress",
+           "supra_bf_beamform_bmode")
 
 
 class SupraError(RuntimeError):
@@ -105,6 +106,8 @@ def lib():
         L.supra_bf_beamform_lines.restype = C.c_int
         L.supra_bf_log_compress.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]
         L.supra_bf_log_compress.restype = C.c_int
+        L.supra_bf_beamform_bmode.argtypes = [vp, vp, C.c_int32, vp, vp, vp]
+        L.supra_bf_beamform_bmode.restype = C.c_int
         _lib = L
     return _lib
 
@@ -207,6 +210,12 @@ class SupraBF:
         """Log compression of a line range against frame_max (or the fixed reference)."""
         _check(lib().supra_bf_log_compress(self.h, _ptr(env), frames, line_first, line_count,
                                            _ptr(frame_max), _ptr(line_img), _stream(stream)))
+
+    def beamform_bmode(self, raw, frames: int, img, mask=None, stream=None):
+        """raw -> B-mode in one call (DAS + envelope, log compression inside
+        scan conversion); img as for scanconvert."""
+        _check(lib().supra_bf_beamform_bmode(self.h, _ptr(raw), frames, _ptr(img), _ptr(mask),
+                                             _stream(stream)))
 
     def scanconvert(self, line_img, frames: int, img, mask=None, stream=None):
         _check(lib().supra_bf_scanconvert(self.h, _ptr(line_img), frames, _ptr(img), _ptr(mask),

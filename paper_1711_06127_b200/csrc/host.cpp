@@ -745,8 +745,9 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   }
   const DasShape sh = das_shape(h->frames_per_cta, h->S, maxF, h->entries_per_group, cfg->fir_taps);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
-  if (e == cudaSuccess && cfg->reference_mode == SUPRA_REF_FRAME_MAX && cfg->line_output_type == SUPRA_T_U8)
-    e = cudaMalloc((void**)&h->d_env, sizeof(float) * (size_t)maxF * h->L * h->S);
+  // f32 line-domain scratch [maxF][L][S/dec]: the envelope of a frame-max
+  // call with a u8 line image, and supra_bf_beamform_bmode's envelope / y
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_env, sizeof(float) * (size_t)maxF * h->L * h->Sd);
   if (e != cudaSuccess) {
     free_all(h);
     delete h;
@@ -783,8 +784,11 @@ supra_status supra_bf_info(supra_bf_t h, int64_t* info8) {
 
 // env_ext != NULL: envelope-only mode for a line range (supra_bf_beamform_lines):
 // the envelope goes to env_ext, per-frame maxima to fmax_ext, no log pass.
+// y_ext != NULL (fixed reference only): the log-compressed line image goes
+// to y_ext as f32 whatever line_output_type is (supra_bf_beamform_bmode).
 static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int line0, int nlines, float* rf,
-                            void* line_img, float* env_ext, float* fmax_ext, cudaStream_t st) {
+                            void* line_img, float* env_ext, float* fmax_ext, cudaStream_t st,
+                            float* y_ext = nullptr) {
   const supra_bf_config& c = h->cfg;
   DasArgs a{};
   a.line0 = line0;
@@ -827,7 +831,11 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   }
   fill_log(h, a.ref_fixed, a.log_k1, a.log_k0);
   a.y_type = c.line_output_type;
-  if (env_ext) {
+  if (y_ext) {
+    a.do_epilogue = 1;
+    a.y_out = y_ext;
+    a.y_type = SUPRA_T_F32;
+  } else if (env_ext) {
     a.do_epilogue = 1;
     a.ref_fixed = 0;
     a.env_out = env_ext;
@@ -1023,22 +1031,14 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float* rf, int32_t frames
   return check_launch(launch_finalize(fa, st), "finalize kernel");
 }
 
-supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t frames, void* img, uint8_t* mask,
-                                  void* stream) {
-  g_err.clear();
-  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
-  if (frames < 0 || frames > h->cfg.max_frames_per_call)
-    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
-  if (!line_img || !img) return fail(SUPRA_E_STRUCT, "line_img and img must not be NULL");
-  if (frames == 0) return SUPRA_OK;
-  DeviceGuard dg(h->cfg.device);
-  const int dev = h->cfg.device;
-  if (!is_device_ptr(line_img, dev) || !is_device_ptr(img, dev) || (mask && !is_device_ptr(mask, dev)))
-    return fail(SUPRA_E_STRUCT, "line_img / img / mask are not device memory of device %d", dev);
+static supra_status run_sc(supra_bf_t h, const void* line_img, int in_type, const unsigned* frame_max,
+                           int32_t frames, void* img, uint8_t* mask, cudaStream_t st) {
   const supra_bf_config& c = h->cfg;
   ScArgs a{};
   a.line_img = line_img;
-  a.in_type = c.line_output_type;
+  a.in_type = in_type;
+  a.frame_max = frame_max;
+  a.DR_k = (float)(20.0 * std::log10(2.0) / c.dynamic_range_db);
   a.F = frames;
   a.Lx = c.num_lines_x;
   a.Ly = c.num_lines_y;
@@ -1062,13 +1062,53 @@ supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t fr
   a.ent = h->d_ent;
   a.is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
   // bulk-copy staging of the slab: 16-byte aligned line segments
-  a.slab_tma = (c.sc_kind == SUPRA_SC_LINEAR_2D && h->sc_tiled && c.line_output_type == SUPRA_T_F32 &&
+  a.slab_tma = (c.sc_kind == SUPRA_SC_LINEAR_2D && h->sc_tiled && in_type == SUPRA_T_F32 &&
                 (h->Sd % 4) == 0 && ((uintptr_t)line_img & 15) == 0)
                    ? 1
                    : 0;
-  cudaStream_t st = (cudaStream_t)stream;
   if (c.sc_kind == SUPRA_SC_LINEAR_2D) return check_launch(launch_sc_linear(a, st), "sc_linear kernel");
   return check_launch(launch_sc_table(a, st), "sc_table kernel");
+}
+
+supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t frames, void* img, uint8_t* mask,
+                                  void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (!line_img || !img) return fail(SUPRA_E_STRUCT, "line_img and img must not be NULL");
+  if (frames == 0) return SUPRA_OK;
+  DeviceGuard dg(h->cfg.device);
+  const int dev = h->cfg.device;
+  if (!is_device_ptr(line_img, dev) || !is_device_ptr(img, dev) || (mask && !is_device_ptr(mask, dev)))
+    return fail(SUPRA_E_STRUCT, "line_img / img / mask are not device memory of device %d", dev);
+  return run_sc(h, line_img, h->cfg.line_output_type, nullptr, frames, img, mask, (cudaStream_t)stream);
+}
+
+supra_status supra_bf_beamform_bmode(supra_bf_t h, const void* raw, int32_t frames, void* img, uint8_t* mask,
+                                     void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (!raw || !img) return fail(SUPRA_E_STRUCT, "raw and img must not be NULL");
+  if (frames == 0) return SUPRA_OK;
+  if ((uintptr_t)raw & 15) return fail(SUPRA_E_STRUCT, "raw must be a 16-byte aligned device pointer");
+  DeviceGuard dg(h->cfg.device);
+  const int dev = h->cfg.device;
+  if (!is_device_ptr(raw, dev) || !is_device_ptr(img, dev) || (mask && !is_device_ptr(mask, dev)))
+    return fail(SUPRA_E_STRUCT, "raw / img / mask are not device memory of device %d", dev);
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return fail(SUPRA_E_CUDA, "pending CUDA error: %s", cudaGetErrorString(pe));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool fixed = h->cfg.reference_mode == SUPRA_REF_FIXED;
+  // DAS + envelope (frame max) into the handle's f32 scratch -- or, with a
+  // fixed reference, DAS + envelope + log straight into it -- then scan
+  // conversion from the scratch (log-compressing each corner on load)
+  supra_status s = run_das(h, raw, frames, 0, h->L, nullptr, nullptr, fixed ? nullptr : h->d_env,
+                           fixed ? nullptr : (float*)h->d_frame_max, st, fixed ? h->d_env : nullptr);
+  if (s != SUPRA_OK) return s;
+  return run_sc(h, h->d_env, SUPRA_T_F32, fixed ? nullptr : h->d_frame_max, frames, img, mask, st);
 }
 
 supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t* valid, int32_t* idx) {

@@ -172,6 +172,12 @@ struct ScArgs {
   const ScRow* rows;     // [nz*ny]
   const ScEntry* ent;
   int is3d;
+  // non-NULL: line_img holds the envelope (f32) and every interpolation
+  // corner is log-compressed on load against frame_max[f] (float bits),
+  // y = clamp(1 + DR_k (log2 env - log2 ref), 0, 1) -- finalize_kernel's
+  // expression, so the image equals finalize + scan conversion bitwise
+  const unsigned* frame_max;
+  float DR_k;
 };
 
 #ifdef __CUDACC__

@@ -21,6 +21,12 @@ __device__ __forceinline__ float load_y(const void* p, int type, size_t i) {
   return __ldg((const float*)p + i);
 }
 
+// log compression of an envelope sample against log2(ref) (finalize_kernel's
+// expression; ref = 0: all-zero frame -> 0)
+__device__ __forceinline__ float y_of_env(float e, float ref, float lref, float DR_k) {
+  return (e > 0.f && ref > 0.f) ? fminf(fmaxf(fmaf(DR_k, lg2_approx(e) - lref, 1.f), 0.f), 1.f) : 0.f;
+}
+
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src)
@@ -154,10 +160,25 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a, in
       __syncthreads();
     }
     // depth lerp of this warp's lines: lane = output row; rows without a
-    // valid k0 are zero
+    // valid k0 are zero.  With frame_max the slab holds the envelope and each
+    // corner is log-compressed first (y_of_env).
+    float ref = 0.f, lref = 0.f;
+    if (a.frame_max) {
+      ref = __uint_as_float(a.frame_max[f]);
+      lref = ref > 0.f ? lg2_approx(ref) : 0.f;
+    }
     for (int j = 0; j < wnl; j++) {
       const float* y = slab[b] + (wl0 + j) * kstride - (use_tma ? kal : kmin);
-      if (lane < rows) tz[lane * TZS + j] = az.i0 >= 0 ? fmaf(az.f, y[az.i0 + 1] - y[az.i0], y[az.i0]) : 0.f;
+      if (lane < rows && az.i0 >= 0) {
+        float y0 = y[az.i0], y1 = y[az.i0 + 1];
+        if (a.frame_max) {
+          y0 = y_of_env(y0, ref, lref, a.DR_k);
+          y1 = y_of_env(y1, ref, lref, a.DR_k);
+        }
+        tz[lane * TZS + j] = fmaf(az.f, y1 - y0, y0);
+      } else if (lane < rows) {
+        tz[lane * TZS + j] = 0.f;
+      }
     }
     __syncwarp();
     if (use_tma && lane == 0)
@@ -197,6 +218,12 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a, in
 __global__ void __launch_bounds__(256) sc_linear_direct_kernel(const ScArgs a) {
   const size_t n = (size_t)a.nz * a.nx;
   const int f = blockIdx.y;
+  const float ref = a.frame_max ? __uint_as_float(a.frame_max[f]) : 0.f;
+  const float lref = ref > 0.f ? lg2_approx(ref) : 0.f;
+  auto load_y = [&](const void* p, int type, size_t i) {
+    const float v = ::supra::load_y(p, type, i);
+    return a.frame_max ? y_of_env(v, ref, lref, a.DR_k) : v;
+  };
   for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (size_t)gridDim.x * blockDim.x) {
     const int iz = (int)(p / a.nx), ix = (int)(p - (size_t)iz * a.nx);
     const ScAxis ax = a.ax[ix], az = a.az[iz];
@@ -217,6 +244,12 @@ __global__ void __launch_bounds__(256) sc_linear_direct_kernel(const ScArgs a) {
 // grid (nz*ny, F); block 256 looping over x.
 __global__ void __launch_bounds__(256) sc_table_kernel(const ScArgs a) {
   const int r = blockIdx.x, f = blockIdx.y;
+  const float ref = a.frame_max ? __uint_as_float(a.frame_max[f]) : 0.f;
+  const float lref = ref > 0.f ? lg2_approx(ref) : 0.f;
+  auto load_y = [&](const void* p, int type, size_t i) {
+    const float v = ::supra::load_y(p, type, i);
+    return a.frame_max ? y_of_env(v, ref, lref, a.DR_k) : v;
+  };
   const ScRow row = a.rows[r];
   const size_t S = (size_t)a.S, LS = (size_t)a.Lx * a.S;
   const size_t fbase = (size_t)f * a.Ly * LS;

@@ -469,3 +469,26 @@ def test_c2_sixteen_frame_batch_epilogue(over):
             assert np.max(np.abs(y_g[f].astype(int) - oracle.to_u8(y_o).astype(int))) <= 1
         else:
             assert db_err(y_g[f], y_o) <= DB_TOL, f
+
+
+# ----------------------- one-call raw -> B-mode (log compression inside SC)
+@pytest.mark.parametrize("name,F,over", [
+    ("C2", 16, dict(sc_output_type=configs.T_U8)),          # linear, tiled SC, frame max
+    ("C2", 3, dict()),                                      # f32 image
+    ("C3", 2, dict(sc_output_type=configs.T_U8)),           # sector table SC
+    ("C1", 1, dict(reference_mode=configs.REF_FIXED, reference_value=3000.0)),
+    ("C1", 1, dict(decimation=2)),
+])
+def test_beamform_bmode_equals_two_calls(name, F, over):
+    w = configs.CONFIGS[name](**over)
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    li = torch.empty((F, w.L, w.S // w.decimation), dtype=torch.float32, device="cuda")
+    bf2 = SupraBF(w.replace(line_output_type=configs.T_F32), max_frames=F)
+    img_a, mask_a = bf2.empty_img(F), bf2.empty_mask()
+    bf2.beamform(raw, F, line_img=li)
+    bf2.scanconvert(li, F, img_a, mask_a)
+    img_b, mask_b = bf.empty_img(F), bf.empty_mask()
+    bf.beamform_bmode(raw, F, img_b, mask_b)
+    torch.cuda.synchronize()
+    assert torch.equal(img_a, img_b) and torch.equal(mask_a, mask_b)
