@@ -66,6 +66,10 @@ def test_c1_point_target_full_chain():
     dict(reference_mode=configs.REF_FIXED, reference_value=5000.0),
     dict(interpolation=configs.INTERP_NEAREST),
     dict(interpolation=configs.INTERP_NEAREST, window=configs.WIN_HAMMING, t0_s=1e-7),
+    dict(fir_taps=129),                       # longest FIR (P = 64)
+    dict(fir_taps=1),                         # degenerate FIR: env = 2|RF| scaled by the one tap
+    dict(f_number=0.02),                      # whole array from the first samples
+    dict(f_number=6.0),                       # tiny aperture: N(k) = 0 for most shallow k
 ])
 def test_c1_variants(over):
     w = configs.c1(**over)
