@@ -346,6 +346,7 @@ def main():
     if not args.no_secondary:
         secondary = secondary_3d(local, world, rank)
         secondary.update(secondary_paper3d(local, world, rank))
+        secondary.update(secondary_sector(local, world, rank))
         secondary.update(secondary_table1(local, world, rank))
 
     if rank == 0:
@@ -486,6 +487,48 @@ def secondary_paper3d(dev_index: int, world: int = 1, rank: int = 0, vols: int =
     del raw, li, img
     torch.cuda.empty_cache()
     return out
+
+
+def secondary_sector(dev_index: int, world: int = 1, rank: int = 0, frames: int = 16):
+    """Frames/s on BASELINE.json configs[2] = C3: phased 128-element probe,
+    192 steered lines over 60 deg, 4096 samples, sector scan conversion to
+    512 x 512 u8; ``frames`` per call per rank (the config's 16-frame
+    batch), DAS + envelope/log + scan conversion, device-timed."""
+    import torch
+    import torch.distributed as dist
+    from synth import configs
+    from paper_1711_06127_b200 import SupraBF
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from gpu_util import raw_frames
+    dev = torch.device(f"cuda:{dev_index}")
+    w = configs.c3(sc_output_type=configs.T_U8)
+    raw = raw_frames(w, frames, device=dev)
+    bf = SupraBF(w, device=dev_index, max_frames=frames)
+    li, img = bf.empty_line_img(frames), bf.empty_img(frames)
+
+    def call():
+        bf.beamform(raw, frames, line_img=li)
+        bf.scanconvert(li, frames, img)
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        call()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / 10], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    bf.close()
+    del raw, li, img
+    torch.cuda.empty_cache()
+    return {"C3": {"value": frames * world * 1000.0 / ms, "unit": "frames/s", "ms_per_call": ms,
+                   "frames_per_call_per_rank": frames, "scaling": "weak"}}
 
 
 # The paper's own 2D benchmark rows (Table 1, P:329-332): GeForce GTX 1080
