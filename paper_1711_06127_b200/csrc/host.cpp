@@ -818,7 +818,13 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.rf = rf;
   a.do_epilogue = line_img != nullptr;
   // measurement only: 1 = TMA pipeline without the tap loop, 2 = tap loop without TMA
+#ifdef SUPRA_DEV_KNOBS
+  // measurement builds only (python -m paper_1711_06127_b200.build --variant=dev -DSUPRA_DEV_KNOBS):
+  // SUPRA_BF_DEBUG=1 skips the tap loop, =2 the TMA staging
   a.debug_skip = std::getenv("SUPRA_BF_DEBUG") ? std::atoi(std::getenv("SUPRA_BF_DEBUG")) : 0;
+#else
+  a.debug_skip = 0;
+#endif
   a.fir = h->d_fir;
   a.fir_taps = c.fir_taps;
   a.nbands = h->nbands;
