@@ -496,3 +496,23 @@ def test_beamform_bmode_equals_two_calls(name, F, over):
     bf.beamform_bmode(raw, F, img_b, mask_b)
     torch.cuda.synchronize()
     assert torch.equal(img_a, img_b) and torch.equal(mask_a, mask_b)
+
+
+def test_c3_bench_launch_configuration():
+    """C3 as the bench times it: 16 frames per call (FB = 16, four 1024-sample
+    depth passes with carried FIR halos, row-cut windows), u8 sector B-mode;
+    frames 0 and 15 vs the oracle chain."""
+    w = configs.c3(sc_output_type=configs.T_U8)
+    F = 16
+    raw = raw_frames(w, F)
+    bf = SupraBF(w, max_frames=F)
+    rf_g, y_g = run_gpu(bf, raw, F)
+    img = bf.empty_img(F)
+    bf.scanconvert(torch.from_numpy(y_g).cuda(), F, img)
+    torch.cuda.synchronize()
+    for f in (0, 15):
+        e_rf, e_db, _, env_o = check_frame(w, raw[f].cpu().numpy(), rf_g[f], y_g[f])
+        assert e_rf <= RF_TOL and e_db <= DB_TOL, (f, e_rf, e_db)
+        y_o, _ = oracle.log_compress(env_o, 50.0)
+        img_o, _ = oracle.scan_convert(w, y_o)
+        assert np.max(np.abs(img[f].cpu().numpy().astype(int) - oracle.to_u8(img_o).astype(int))) <= 1
