@@ -73,6 +73,7 @@ __host__ __device__ inline WarpLayout warp_layout(int S, int rows, int P) {
 struct EntryCtx {
   float Ah, B, cu;  // |q|^2/2, d.q (samples), 2 F rho / dr (u = cu / k)
   int wsl;          // ws + magic bits - lane:  idx = bits(floor tf) - wsl + 32 t
+  uint32_t abase;   // sbase - 2 wsl: the stage address of x[i0] is 2 bits(floor tf) + abase + 64 t
   int kenter;
   uint32_t sbase;   // shared address of the entry's stage
 };
@@ -98,8 +99,7 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
   float2 delta = split_delay2(c.Ah, c.B, h, hh);
   if (MODE >= 1) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));  // t0 (+ 1/2 for nearest)
   const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
-  const int idx0 = __float_as_int(tf.x) - c.wsl + 64 * PP;
-  const int idx1 = __float_as_int(tf.y) - c.wsl + 64 * PP + 32;
+
   const float2 fr = sub2(delta, sub2(tf, make_float2(kFloorMagic, kFloorMagic)));
   const float2 rk = rkt[PP * 32 + lane];
   float2 u = __fmul2_rn(make_float2(c.cu, c.cu), rk);
@@ -120,12 +120,14 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
   }
   // linear interpolation v = x0 + f (x1 - x0), then acc += w v: 3 packed
   // FP32 ops per pair (the FP32 pipe, not issue, bounds this kernel)
-  const uint32_t p0 = c.sbase + 2u * (uint32_t)idx0, p1 = c.sbase + 2u * (uint32_t)idx1;
-  const float2 x0 = make_float2(lds_s16f(p0, 0), lds_s16f(p1, 0));
+  // one IMAD per tap for the address; the tile offset is a load immediate
+  const uint32_t p0 = 2u * (uint32_t)__float_as_int(tf.x) + c.abase;
+  const uint32_t p1 = 2u * (uint32_t)__float_as_int(tf.y) + c.abase;
+  const float2 x0 = make_float2(lds_s16f(p0, 128 * PP), lds_s16f(p1, 128 * PP + 64));
   if constexpr (MODE == 2) {  // nearest sample x~[floor(tau + 1/2)]
     acc = __ffma2_rn(w, x0, acc);
   } else {
-    const float2 x1 = make_float2(lds_s16f(p0, 2), lds_s16f(p1, 2));
+    const float2 x1 = make_float2(lds_s16f(p0, 128 * PP + 2), lds_s16f(p1, 128 * PP + 66));
     const float2 v = __ffma2_rn(fr, sub2(x1, x0), x0);
     acc = __ffma2_rn(w, v, acc);
   }
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     c.kenter = e.kenter;
     c.wsl = ws + kFloorMagicBits - lane;
     c.sbase = smem_u32(ring + (size_t)(warp * NSW + slot) * SB);
+    c.abase = c.sbase - 2u * (uint32_t)c.wsl;
     if (a.debug_skip != 2) mbar_wait(&full[warp * kMaxWarpStages + slot], phase);
     // opaque per-entry copy of the lane coordinate: keeps the compiler from
     // hoisting the 2 NP per-pair (h, h^2) constants out of the entry loop
