@@ -90,7 +90,10 @@ __device__ __forceinline__ int entry_ws(const DasEntry& e, const float4& dir, fl
 }
 
 // Tile pair (2p, 2p+1): output samples k = 64 p + lane and k + 32.
-template <int PP, bool HANN, int MODE>
+// FIRST: the entry's first group of tile pairs (it holds k_enter): the only
+// one with non-member samples, so the only one needing the aperture clamp
+// (Hann) or the k >= k_enter predicate (other windows).
+template <int PP, bool HANN, int MODE, bool FIRST>
 __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, const float2* rkt, int lane,
                                          float2 lanef, float2& acc) {
   const float2 h = __ffma2_rn(lanef, make_float2(0.5f, 0.5f), make_float2(32.0f * PP, 32.0f * PP + 16.0f));
@@ -105,8 +108,10 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
   float2 u = __fmul2_rn(make_float2(c.cu, c.cu), rk);
   float2 w;
   if constexpr (HANN) {
-    u.x = fminf(u.x, 1.0f);
-    u.y = fminf(u.y, 1.0f);
+    if constexpr (FIRST) {
+      u.x = fminf(u.x, 1.0f);
+      u.y = fminf(u.y, 1.0f);
+    }
     const float2 v = __ffma2_rn(u, make_float2(-1.57079632679f, -1.57079632679f),
                                 make_float2(1.57079632679f, 1.57079632679f));
     const float2 sn = make_float2(__sinf(v.x), __sinf(v.y));
@@ -115,8 +120,10 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
     const int k = 64 * PP + lane;
     w = __ffma2_rn(make_float2(__cosf(3.14159265358979f * u.x), __cosf(3.14159265358979f * u.y)),
                    make_float2(a.win_b, a.win_b), make_float2(a.win_a, a.win_a));
-    w.x = k >= c.kenter ? w.x : 0.f;
-    w.y = k + 32 >= c.kenter ? w.y : 0.f;
+    if constexpr (FIRST) {
+      w.x = k >= c.kenter ? w.x : 0.f;
+      w.y = k + 32 >= c.kenter ? w.y : 0.f;
+    }
   }
   // linear interpolation v = x0 + f (x1 - x0), then acc += w v: 3 packed
   // FP32 ops per pair (the FP32 pipe, not issue, bounds this kernel)
@@ -140,31 +147,44 @@ __device__ __forceinline__ void pair_tap(const DasArgs& a, const EntryCtx& c, co
 // serialises the pairs' dependency chains); the up to kGroup - 1 extra
 // leading pairs carry zero weight (k < k_enter).
 constexpr int kGroup = 4;
-template <int G0, int NP, bool HANN, int MODE>
+template <int G0, int NP, bool HANN, int MODE, bool FIRST>
 __device__ __forceinline__ void pair_group(const DasArgs& a, const EntryCtx& c, const float2* rkt, int lane,
                                            float2 lanef, float2* acc) {
   constexpr int q = G0 * kGroup < NP ? G0 * kGroup : 0;
-  pair_tap<q + 0, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 0]);
-  pair_tap<q + 1, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 1]);
-  pair_tap<q + 2, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 2]);
-  pair_tap<q + 3, HANN, MODE>(a, c, rkt, lane, lanef, acc[q + 3]);
+  pair_tap<q + 0, HANN, MODE, FIRST>(a, c, rkt, lane, lanef, acc[q + 0]);
+  pair_tap<q + 1, HANN, MODE, FIRST>(a, c, rkt, lane, lanef, acc[q + 1]);
+  pair_tap<q + 2, HANN, MODE, FIRST>(a, c, rkt, lane, lanef, acc[q + 2]);
+  pair_tap<q + 3, HANN, MODE, FIRST>(a, c, rkt, lane, lanef, acc[q + 3]);
 }
-#define SUPRA_GROUP(g)                                                              \
-  case g:                                                                          \
-    if constexpr ((g) * kGroup < NP) pair_group<(g), NP, HANN, MODE>(a, c, rkt, lane, lanef, acc); \
+#define SUPRA_FIRST(g)                                                                         \
+  case g:                                                                                      \
+    if constexpr ((g) * kGroup < NP) pair_group<(g), NP, HANN, MODE, true>(a, c, rkt, lane, lanef, acc); \
+    break;
+#define SUPRA_REST(g)                                                                          \
+  case g:                                                                                      \
+    if constexpr ((g) * kGroup < NP) pair_group<(g), NP, HANN, MODE, false>(a, c, rkt, lane, lanef, acc); \
     [[fallthrough]];
+// The entry's first group (membership handled), then the remaining groups
+// by fall-through (all members: no clamp / predicate).
 template <int NP, bool HANN, int MODE>
 __device__ __forceinline__ void entry_pairs(int p0, const DasArgs& a, const EntryCtx& c, const float2* rkt, int lane,
                                             float2 lanef, float2* acc) {
   static_assert(NP % kGroup == 0 && NP / kGroup <= 8, "pair groups");
-  switch (p0 / kGroup) {
-    SUPRA_GROUP(0) SUPRA_GROUP(1) SUPRA_GROUP(2) SUPRA_GROUP(3) SUPRA_GROUP(4) SUPRA_GROUP(5) SUPRA_GROUP(6)
-    SUPRA_GROUP(7)
+  const int g0 = p0 / kGroup;
+  switch (g0) {
+    SUPRA_FIRST(0) SUPRA_FIRST(1) SUPRA_FIRST(2) SUPRA_FIRST(3) SUPRA_FIRST(4) SUPRA_FIRST(5) SUPRA_FIRST(6)
+    SUPRA_FIRST(7)
+    default:
+      break;
+  }
+  switch (g0 + 1) {
+    SUPRA_REST(1) SUPRA_REST(2) SUPRA_REST(3) SUPRA_REST(4) SUPRA_REST(5) SUPRA_REST(6) SUPRA_REST(7)
     default:
       break;
   }
 }
-#undef SUPRA_GROUP
+#undef SUPRA_FIRST
+#undef SUPRA_REST
 
 }  // namespace
 
