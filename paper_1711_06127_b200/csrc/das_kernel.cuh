@@ -127,7 +127,7 @@ struct Acc {
 // Per-tile tap geometry: index of x[i0] in the staged window and the two
 // interpolation weights.
 struct TapGeo {
-  int idx;
+  uint32_t addr;  // shared byte address of x[i0] minus the tile's 512 m (a load immediate)
   float w0, w1;
 };
 
@@ -136,18 +136,19 @@ __host__ __device__ constexpr int tile_gran(int NT) { return NT <= 8 ? 1 : 2; }
 
 // Accumulate one tile's tap for all FB frames (per frame pair: 4 sign-
 // extending LDS.S16 + I2FP, 2 FFMA2; frames at immediate offsets).
-template <int FB, int NT>
-__device__ __forceinline__ void tile_accumulate(const TapGeo& g, const unsigned short* st, float2* accp) {
+template <int FB, int NT, int M>
+__device__ __forceinline__ void tile_accumulate(const TapGeo& g, float2* accp) {
   constexpr int FR = (NT * 8 + 2) * kRowSamples;
-  int idx = g.idx;
-  // opaque copy: keeps one materialised index so the FB loads below use
+  constexpr int MO = 2 * M * kTileK;  // the tile's offset, folded into the load immediates
+  uint32_t pa = g.addr;
+  // opaque copy: keeps one materialised address so the FB loads below use
   // immediate offsets instead of one address add each
-  asm("mov.b32 %0, %0;" : "+r"(idx));
-  const uint32_t pa = smem_u32(st) + 2u * (uint32_t)idx;
+  asm("mov.b32 %0, %0;" : "+r"(pa));
 #pragma unroll
   for (int q = 0; q < FB / 2; q++) {
-    const float2 x0 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR), lds_s16f(pa, 2 * (2 * q + 1) * FR));
-    const float2 x1 = make_float2(lds_s16f(pa, 2 * (2 * q) * FR + 2), lds_s16f(pa, 2 * (2 * q + 1) * FR + 2));
+    const float2 x0 = make_float2(lds_s16f(pa, MO + 2 * (2 * q) * FR), lds_s16f(pa, MO + 2 * (2 * q + 1) * FR));
+    const float2 x1 =
+        make_float2(lds_s16f(pa, MO + 2 * (2 * q) * FR + 2), lds_s16f(pa, MO + 2 * (2 * q + 1) * FR + 2));
     accp[q] = __ffma2_rn(make_float2(g.w0, g.w0), x0, accp[q]);
     accp[q] = __ffma2_rn(make_float2(g.w1, g.w1), x1, accp[q]);
   }
@@ -159,7 +160,7 @@ __device__ __forceinline__ void tile_accumulate(const TapGeo& g, const unsigned 
 // computed but never stored; their taps stay inside the window.
 template <int NT, int M0, bool T0>
 __device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4& r, int kenter, int wsm,
-                                           int kt, int k0, float kt0f) {
+                                           uint32_t sbase, int kt, int k0, float kt0f) {
   const int k = k0 + m * kTileK + kt;
   const bool mem = !(m < M0 + tile_gran(NT)) || k >= kenter;
   const float kf = kt0f + (float)(m * kTileK);
@@ -168,21 +169,22 @@ __device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4
   float delta = split_delay(r.x, r.y, h, h2);
   if (T0) delta += a.t0fs;
   const float tf = __fadd_rd(delta, kFloorMagic);
-  const int idx = __float_as_int(tf) - wsm + m * kTileK;  // i0 - ws  (wsm = ws + magic - k0 - kt)
+  // &x[i0] - 512 m = sbase + 2 (i0 - ws) - 512 m = 2 bits(tf) + (sbase - 2 wsm)  (wsm = ws + magic - k0 - kt)
+  const uint32_t ad = 2u * (uint32_t)__float_as_int(tf) + (sbase - 2u * (uint32_t)wsm);
   const float fr = (delta - (tf - kFloorMagic)) * a.fr_scale;
   float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
   w = mem ? w : 0.f;
   // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
   const float w1 = w * fr;
-  return TapGeo{mem ? idx : 0, w - w1, w1};
+  return TapGeo{mem ? ad : sbase - 2u * (uint32_t)(m * kTileK), w - w1, w1};
 }
 
 // Geometry of tiles m, m+1 together in packed f32x2 (FFMA2 / FADD2.RM /
 // FMUL2: about 40 % fewer issued instructions than two scalar tiles; the
 // per-lane arithmetic is the same, so results are identical).
 template <int NT, int M0, bool T0>
-__device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4& r, int kenter, int wsm, int kt,
-                                          int k0, float kt0f, TapGeo& g0, TapGeo& g1) {
+__device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4& r, int kenter, int wsm,
+                                          uint32_t sbase, int kt, int k0, float kt0f, TapGeo& g0, TapGeo& g1) {
   const int ka = k0 + m * kTileK + kt;
   const bool mem0 = !(m < M0 + tile_gran(NT)) || ka >= kenter;
   const bool mem1 = !(m + 1 < M0 + tile_gran(NT)) || ka + kTileK >= kenter;
@@ -193,8 +195,8 @@ __device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4&
   float2 delta = split_delay2(r.x, r.y, h, h2);
   if (T0) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));
   const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
-  const int idx0 = __float_as_int(tf.x) - wsm + m * kTileK;
-  const int idx1 = __float_as_int(tf.y) - wsm + (m + 1) * kTileK;
+  const uint32_t ab = sbase - 2u * (uint32_t)wsm;
+  const uint32_t ad0 = 2u * (uint32_t)__float_as_int(tf.x) + ab, ad1 = 2u * (uint32_t)__float_as_int(tf.y) + ab;
   const float2 fr = __fmul2_rn(sub2(delta, sub2(tf, make_float2(kFloorMagic, kFloorMagic))),
                                make_float2(a.fr_scale, a.fr_scale));
   const float2 u = __fmul2_rn(make_float2(r.z, r.z),
@@ -205,8 +207,30 @@ __device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4&
   w.y = mem1 ? w.y : 0.f;
   const float2 w1 = __fmul2_rn(w, fr);
   const float2 w0 = sub2(w, w1);
-  g0 = TapGeo{mem0 ? idx0 : 0, w0.x, w1.x};
-  g1 = TapGeo{mem1 ? idx1 : 0, w0.y, w1.y};
+  g0 = TapGeo{mem0 ? ad0 : sbase - 2u * (uint32_t)(m * kTileK), w0.x, w1.x};
+  g1 = TapGeo{mem1 ? ad1 : sbase - 2u * (uint32_t)((m + 1) * kTileK), w0.y, w1.y};
+}
+
+// Tile pairs (M, M+1), (M+2, M+3), ... of an entry (compile-time recursion so
+// the tile index is a template argument: its offset is a load immediate).
+template <int FB, int NT, int M0, bool T0, int M>
+__device__ __forceinline__ void tile_pairs(const DasArgs& a, const float4& r, int kenter, int wsm, uint32_t sbase,
+                                           int kt, int k0, float kt0f, Acc<FB, NT>& acc) {
+  if constexpr (M + 1 < NT) {
+    TapGeo g0, g1;
+    tile_geo2<NT, M0, T0>(M, a, r, kenter, wsm, sbase, kt, k0, kt0f, g0, g1);
+    if constexpr (FB == 1) {
+      constexpr int o0 = 2 * M * kTileK, o1 = 2 * (M + 1) * kTileK;
+      const float2 x0 = make_float2(lds_s16f(g0.addr, o0), lds_s16f(g1.addr, o1));
+      const float2 x1 = make_float2(lds_s16f(g0.addr, o0 + 2), lds_s16f(g1.addr, o1 + 2));
+      acc.s2[M / 2] = __ffma2_rn(make_float2(g0.w0, g1.w0), x0, acc.s2[M / 2]);
+      acc.s2[M / 2] = __ffma2_rn(make_float2(g0.w1, g1.w1), x1, acc.s2[M / 2]);
+    } else {
+      tile_accumulate<FB, NT, M>(g0, acc.p[M]);
+      tile_accumulate<FB, NT, M + 1>(g1, acc.p[M + 1]);
+    }
+    tile_pairs<FB, NT, M0, T0, M + 2>(a, r, kenter, wsm, sbase, kt, k0, kt0f, acc);
+  }
 }
 
 // One aperture entry, output tiles M0 .. NT-1 of the pass (straight-line):
@@ -216,32 +240,18 @@ template <int FB, int NT, int M0, bool T0>
 __device__ __forceinline__ void entry_tiles(const DasArgs& a, const float4& r, int kenter, int wsm,
                                             const unsigned short* st, int kt, int k0, float kt0f,
                                             Acc<FB, NT>& acc) {
+  const uint32_t sbase = smem_u32(st);
   if constexpr (M0 & 1) {
-    const TapGeo g = tile_geo<NT, M0, T0>(M0, a, r, kenter, wsm, kt, k0, kt0f);
+    const TapGeo g = tile_geo<NT, M0, T0>(M0, a, r, kenter, wsm, sbase, kt, k0, kt0f);
     if constexpr (FB == 1) {
-      const uint32_t pa = smem_u32(st) + 2u * (uint32_t)g.idx;
       float& s1 = acc.s2[M0 / 2].y;
-      s1 = fmaf(g.w0, lds_s16f(pa, 0), s1);
-      s1 = fmaf(g.w1, lds_s16f(pa, 2), s1);
+      s1 = fmaf(g.w0, lds_s16f(g.addr, 2 * M0 * kTileK), s1);
+      s1 = fmaf(g.w1, lds_s16f(g.addr, 2 * M0 * kTileK + 2), s1);
     } else {
-      tile_accumulate<FB, NT>(g, st, acc.p[M0]);
+      tile_accumulate<FB, NT, M0>(g, acc.p[M0]);
     }
   }
-#pragma unroll
-  for (int m = (M0 + 1) & ~1; m < NT; m += 2) {
-    TapGeo g0, g1;
-    tile_geo2<NT, M0, T0>(m, a, r, kenter, wsm, kt, k0, kt0f, g0, g1);
-    if constexpr (FB == 1) {
-      const uint32_t p0 = smem_u32(st) + 2u * (uint32_t)g0.idx, p1 = smem_u32(st) + 2u * (uint32_t)g1.idx;
-      const float2 x0 = make_float2(lds_s16f(p0, 0), lds_s16f(p1, 0));
-      const float2 x1 = make_float2(lds_s16f(p0, 2), lds_s16f(p1, 2));
-      acc.s2[m / 2] = __ffma2_rn(make_float2(g0.w0, g1.w0), x0, acc.s2[m / 2]);
-      acc.s2[m / 2] = __ffma2_rn(make_float2(g0.w1, g1.w1), x1, acc.s2[m / 2]);
-    } else {
-      tile_accumulate<FB, NT>(g0, st, acc.p[m]);
-      tile_accumulate<FB, NT>(g1, st, acc.p[m + 1]);
-    }
-  }
+  tile_pairs<FB, NT, M0, T0, ((M0 + 1) & ~1)>(a, r, kenter, wsm, sbase, kt, k0, kt0f, acc);
 }
 
 template <int FB, int NT, bool T0, int G = 0>
