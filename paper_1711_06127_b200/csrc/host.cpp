@@ -1072,7 +1072,25 @@ static supra_status run_sc(supra_bf_t h, const void* line_img, int in_type, cons
                 (h->Sd % 4) == 0 && ((uintptr_t)line_img & 15) == 0)
                    ? 1
                    : 0;
-  if (c.sc_kind == SUPRA_SC_LINEAR_2D) return check_launch(launch_sc_linear(a, st), "sc_linear kernel");
+  // one 2-D tensor map over the [frames Lx][Sd] f32 line image: a single
+  // TMA per (tile, frame) instead of one bulk copy per line (1-D fallback if
+  // the encode fails)
+  CUtensorMap slab_map;
+  const CUtensorMap* sm = nullptr;
+  if (a.slab_tma && frames > 0) {
+    EncodeTiledFn fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)h->Sd, (cuuint64_t)frames * c.num_lines_x};
+    cuuint64_t strides[1] = {(cuuint64_t)h->Sd * 4};
+    cuuint32_t box[2] = {(cuuint32_t)h->sc_box_k, (cuuint32_t)h->sc_box_l};
+    cuuint32_t es[2] = {1, 1};
+    if (fn && fn(&slab_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(line_img), dims, strides, box,
+                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      sm = &slab_map;
+      a.slab_tma = 2;
+    }
+  }
+  if (c.sc_kind == SUPRA_SC_LINEAR_2D) return check_launch(launch_sc_linear(a, sm, st), "sc_linear kernel");
   return check_launch(launch_sc_table(a, st), "sc_table kernel");
 }
 

@@ -166,7 +166,7 @@ struct ScArgs {
   const int32_t* col_l0;    // [ceil(nx / 256)]: first line the column tile touches
   const int32_t* col_nl;    // [ceil(nx / 256)]: lines it touches (0: none valid)
   int tiled;             // 1: tiled separable kernel; 0: direct per-pixel kernel
-  int slab_tma;          // 1: stage the slab with 1-D bulk copies (f32 line image)
+  int slab_tma;          // 1: stage the slab with 1-D bulk copies, 2: one 2-D tensor copy (f32 line image)
   int slab_box_k, slab_box_l;  // staged segment: samples (multiple of 4) x lines
   // table
   const ScRow* rows;     // [nz*ny]
@@ -202,7 +202,7 @@ cudaError_t launch_das_warp(const CUtensorMap& raw_map, const DasArgs& a, cudaSt
 size_t das_smem_bytes(int fb, int nt, int nent_max, int fir_taps);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
-cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st);
+cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaStream_t st);
 cudaError_t launch_sc_table(const ScArgs& a, cudaStream_t st);
 
 }  // namespace supra

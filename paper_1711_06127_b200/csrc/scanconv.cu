@@ -57,7 +57,8 @@ __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) 
 // a per-buffer "empty" mbarrier (8 warp arrivals) gates the refill.
 constexpr int kScWarpLines = kScWarpLinesMax + 1;  // + the zero pair
 template <bool U8OUT>
-__global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a, int fpc) {
+__global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_constant__ CUtensorMap tm,
+                                                              const ScArgs a, int fpc) {
   __shared__ __align__(128) float slab[2][kScMaxLines * kScMaxK];
   constexpr int TZS = kScWarpLines + 1;  // odd row stride: conflict-free row writes
   __shared__ float tzw[8][kScRows * TZS];
@@ -111,9 +112,26 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const ScArgs a, in
         "r"(parity)
         : "memory");
   };
-  // one 1-D bulk copy (TMA, UBLKCP) per line segment [kal, kal + box_k)
-  // (clipped to the record), lanes of warp 0 take lines
+  // slab_tma == 2: ONE 2-D tensor copy (UTMALDG) of the box {box_k samples,
+  // box_l lines} at (kal, f Lx + l0) of the [F Lx][S] line image; lines past
+  // the tile's nl are staged but unused, samples/rows past the image read 0.
+  // slab_tma == 1: one 1-D bulk copy (UBLKCP) per line segment
+  // [kal, kal + box_k) (clipped to the record), lanes of warp 0 take lines.
   auto issue = [&](int f, int b) {
+    if (a.slab_tma == 2) {
+      const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&full[b]);
+      const unsigned bytes =
+          (lane == 0 && kmin >= 0 && nl > 0) ? (unsigned)(a.slab_box_k * a.slab_box_l) * 4u : 0u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+      if (bytes)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"((uint32_t)__cvta_generic_to_shared(slab[b])),
+            "l"(reinterpret_cast<uint64_t>(&tm)), "r"(kal), "r"(f * Lx + l0), "r"(bb)
+            : "memory");
+      return;
+    }
     const float* src = (const float*)a.line_img + (size_t)f * Lx * S;
     const int seg = min(a.slab_box_k, S - kal);
     const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&full[b]);
@@ -286,7 +304,7 @@ __global__ void __launch_bounds__(256) sc_table_kernel(const ScArgs a) {
   }
 }
 
-cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st) {
+cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaStream_t st) {
   if (!a.tiled) {
     dim3 g2(std::min<size_t>(((size_t)a.nz * a.nx + 255) / 256, 148 * 8), a.F);
     sc_linear_direct_kernel<<<g2, 256, 0, st>>>(a);
@@ -295,12 +313,14 @@ cudaError_t launch_sc_linear(const ScArgs& a, cudaStream_t st) {
   // frames per CTA: enough CTAs for ~4 waves of 148 SMs x 4 resident,
   // the rest of the frames walked by each CTA with double-buffered staging
   const long tiles = (long)((a.nx + 255) / 256) * ((a.nz + kScRows - 1) / kScRows);
-  const long want = 148L * 4 * 4;
+  const long want = 148L * 4 * 16;  // ~5 frames per CTA at C2 (measured: 4x: 247, 16x: 242 us / 100 frames)
   int fpc = (int)std::max<long>(1, (tiles * a.F + want - 1) / want);
   fpc = std::min(fpc, a.F);
   dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, (a.F + fpc - 1) / fpc);
-  if (a.out_type == SUPRA_T_U8) sc_linear_tiled_kernel<true><<<grid, 256, 0, st>>>(a, fpc);
-  else sc_linear_tiled_kernel<false><<<grid, 256, 0, st>>>(a, fpc);
+  CUtensorMap none{};
+  const CUtensorMap& tm = slab_map ? *slab_map : none;
+  if (a.out_type == SUPRA_T_U8) sc_linear_tiled_kernel<true><<<grid, 256, 0, st>>>(tm, a, fpc);
+  else sc_linear_tiled_kernel<false><<<grid, 256, 0, st>>>(tm, a, fpc);
   return cudaGetLastError();
 }
 
