@@ -310,10 +310,11 @@ cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaS
     sc_linear_direct_kernel<<<g2, 256, 0, st>>>(a);
     return cudaGetLastError();
   }
-  // frames per CTA: enough CTAs for ~4 waves of 148 SMs x 4 resident,
+  // frames per CTA: enough CTAs for ~8 waves of 148 SMs x 4 resident,
   // the rest of the frames walked by each CTA with double-buffered staging
   const long tiles = (long)((a.nx + 255) / 256) * ((a.nz + kScRows - 1) / kScRows);
-  const long want = 148L * 4 * 16;  // ~5 frames per CTA at C2 (measured: 4x: 247, 16x: 242 us / 100 frames)
+  // (C2, 2-D TMA slab, us per 100 frames: 4 waves 191, 8: 187, 16: 189, 32: 207)
+  const long want = 148L * 4 * 8;
   int fpc = (int)std::max<long>(1, (tiles * a.F + want - 1) / want);
   fpc = std::min(fpc, a.F);
   dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, (a.F + fpc - 1) / fpc);
