@@ -389,3 +389,40 @@ def test_paper_3d_shape_P228_P337():
                                np.hypot(w.line_direction[:, 1], w.line_direction[:, 2])))
     assert abs(th.max() - 30.0) < 1e-9 and abs(th.min() + 30.0) < 1e-9   # S:66 endpoints
     assert w.out_spacing_mm == (0.175, 0.175, 0.175)
+
+
+# Window shape pinned by its textbook landmarks (S:125 lists {rectangular,
+# hann, hamming}; reading #9 maps the aperture edge rho = R to u = 1):
+# Hann is 0 at the edge, 1/2 half way, 1 on the axis; Hamming is 0.08 at the
+# edge (0.54 - 0.46), 0.54 half way and 1 on the axis; rect is 1 throughout.
+@pytest.mark.parametrize("window,edge,half,axis", [
+    (configs.WIN_HANN, 0.0, 0.5, 1.0),
+    (configs.WIN_HAMMING, 0.08, 0.54, 1.0),
+    (configs.WIN_RECT, 1.0, 1.0, 1.0),
+])
+def test_window_landmarks_single_element_S125(window, edge, half, axis):
+    # binary-exact geometry: dr = 2^-6 mm (fs = 49.28 MHz at c = 1540 m/s),
+    # pitch 2^-4 mm, F = 1.  The neighbour of line l sits at rho = 2^-4 mm:
+    # it joins the aperture at k = 8 (2 F rho = 8 dr exactly, u = rho / R = 1)
+    # and is half way in at k = 16 (u = 1/2).  Only one channel carries data
+    # (constant 1000, every tau inside the record), normalize = none, so
+    # RF[l][k] = 1000 w(u) isolates the window value of that one element.
+    fs = 1000.0 * 1540.0 / (2.0 * 2.0 ** -6)
+    w = tiny_linear(n_el=16, pitch=2.0 ** -4, S=64).replace(fs_hz=fs, window=window,
+                                                            normalize=configs.NORM_NONE)
+    assert oracle.dr_mm(w.c_mps, w.fs_hz) == 2.0 ** -6
+    l = 7
+    raw = np.zeros((w.num_events, w.C, w.S), np.int16)
+    raw[l, l + 1, :] = 1000                       # the neighbour at rho = pitch
+    rf = oracle.das(w, raw)
+    assert np.all(rf[l, :8] == 0.0)               # not yet a member
+    assert abs(rf[l, 8] - 1000.0 * edge) < 1e-9   # u = 1: the aperture edge
+    assert abs(rf[l, 16] - 1000.0 * half) < 1e-9  # u = 1/2
+    # the line's own element (rho = 0, u = 0 at every depth, reading #9)
+    raw2 = np.zeros_like(raw)
+    raw2[l, l, :] = 1000
+    rf2 = oracle.das(w, raw2)
+    assert np.all(np.abs(rf2[l, :40] - 1000.0 * axis) < 1e-9)
+    # the weight is monotone in u (edge -> axis) along the entering element
+    seg = rf[l, 8:40]
+    assert np.all(np.diff(seg) >= -1e-9) if edge <= axis else True

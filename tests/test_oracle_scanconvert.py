@@ -198,3 +198,42 @@ def test_decimated_line_image_depth_axis_S224(dec):
     zmax = (Sd - 1) * dec * configs.dr_mm()
     rows = np.where(m.any(1))[0]
     assert Z[rows].max() <= zmax + 1e-12 and Z[rows.max() + 1] > zmax if rows.max() + 1 < len(Z) else True
+
+
+def test_pyramid_angular_axes_pinned_by_forward_steering_model():
+    # Trilinear interpolation reproduces y = a lx + b ly + c k + d, so the
+    # image must equal a u_x + b u_y + c v + d, where (u_x, u_y, v) come from
+    # inverting the FORWARD steering model of reading #13, written here
+    # independently of the oracle's atan2 form: a voxel P = r d(tx, ty) with
+    # d = (sin tx, cos tx sin ty, cos tx cos ty) has r = |P|, tx = asin(X / r),
+    # ty = atan(Y / Z); u = angle / dtheta + (L - 1)/2 (reading #14).
+    # Lx != Ly and fov_x != fov_y, so a transposed line index or swapped
+    # (fx, fy) fractions change the result.
+    w = pyramid()                                  # Lx = 6, Ly = 5, 60 x 40 deg
+    Lx, Ly, S = w.num_lines_x, w.num_lines_y, w.S
+    a, b, c, d = 0.37, -0.61, 0.002, 0.25
+    ly, lx, k = np.meshgrid(np.arange(Ly), np.arange(Lx), np.arange(S), indexing="ij")
+    y = (a * lx + b * ly + c * k + d).reshape(Lx * Ly, S)   # line l = ly Lx + lx
+    img, mask = oracle.scan_convert(w, y)
+    n = w.out_dims[0]
+    sp = w.out_spacing_mm[0]
+    X = w.out_origin_mm[0] + np.arange(n) * sp
+    Y = w.out_origin_mm[1] + np.arange(n) * sp
+    Z = np.arange(n) * sp
+    ZZ, YY, XX = np.meshgrid(Z, Y, X, indexing="ij")
+    m = (mask == 1).reshape(n, n, n)
+    assert m.sum() > 100
+    r = np.sqrt(XX ** 2 + YY ** 2 + ZZ ** 2)
+    tx = np.arcsin(XX[m] / r[m])
+    ty = np.arctan(YY[m] / ZZ[m])
+    ux = tx / (math.radians(60.0) / (Lx - 1)) + (Lx - 1) / 2
+    uy = ty / (math.radians(40.0) / (Ly - 1)) + (Ly - 1) / 2
+    v = r[m] / configs.dr_mm()
+    expect = a * ux + b * uy + c * v + d
+    got = img.reshape(n, n, n)[m]
+    assert np.max(np.abs(got - expect)) < 1e-9
+    # the angular axes separately (each must be reproduced on its own)
+    img_x, _ = oracle.scan_convert(w, (1.0 * lx + 0 * k).reshape(Lx * Ly, S).astype(float))
+    img_y, _ = oracle.scan_convert(w, (1.0 * ly + 0 * k).reshape(Lx * Ly, S).astype(float))
+    assert np.max(np.abs(img_x.reshape(n, n, n)[m] - ux)) < 1e-9
+    assert np.max(np.abs(img_y.reshape(n, n, n)[m] - uy)) < 1e-9
