@@ -318,6 +318,53 @@ def main():
                 "das_ms_per_launch": das_ms, "algorithmic_bytes_per_launch": alg_bytes,
                 "das_share_of_step": das_ms / ms_per_step}
 
+    # N > 1: the same stream without the gather (per-rank
+    # compute rate) and with the line-domain variant (u8 line images, 0.5 MB
+    # per C2 frame instead of the 2.97 MB B-mode, gathered to rank 0; scan
+    # conversion then happens where the images are displayed)
+    multi = None
+    if world > 1:
+        def timed_steps(fn, k):
+            for j in range(3):
+                fn(j)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for j in range(k):
+                fn(3 + j)
+            b.record(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            tt = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt[0])
+
+        def step_ng(_):
+            bf.beamform(raw, F, line_img=li)
+            bf.scanconvert(li, F, img)
+        ms_ng = timed_steps(step_ng, K)
+        bf8 = SupraBF(w.replace(line_output_type=configs.T_U8), device=local, max_frames=F)
+        g8 = OverlappedGather(bf8.empty_line_img(F), dst=0)
+
+        def step_ld(j):
+            bf8.beamform(raw, F, line_img=g8.buffer(j))
+            g8.submit(j)
+
+        def step_ld_drained(j):
+            step_ld(j)
+            if j == 3 + K - 1:
+                g8.drain()
+        ms_ld = timed_steps(step_ld_drained, K)
+        bf8.close()
+        multi = {"no_gather": {"value": F * world * K / (ms_ng / 1000.0), "unit": "frames/s",
+                               "ms_per_step": ms_ng / K,
+                               "what": "beamform + scanconvert on every rank, no collective"},
+                 "line_domain_gather": {"value": F * world * K / (ms_ld / 1000.0), "unit": "frames/s",
+                                        "ms_per_step": ms_ld / K,
+                                        "what": "beamform to u8 line images + NCCL gather of the line "
+                                                "images to rank 0 (no scan conversion)"}}
+
     # end to end: pinned host input -> public API (HostPipeline) -> pinned host B-mode
     e2e = None
     if not args.no_e2e:
@@ -344,10 +391,7 @@ def main():
         r, cores, sample = oracle_frame_rate(w, raw[0].cpu().numpy(), 12.0)
         cpu_baseline = {"value": r, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample}
     if not args.no_secondary:
-        secondary = secondary_3d(local, world, rank)
-        secondary.update(secondary_paper3d(local, world, rank))
-        secondary.update(secondary_sector(local, world, rank))
-        secondary.update(secondary_table1(local, world, rank))
+        secondary = secondary_all(local, world, rank)
 
     if rank == 0:
         line = {
@@ -361,7 +405,7 @@ def main():
                        if world > 1 else "single GPU"},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": K * (info["kernels_per_beamform"] + info["kernels_per_scanconvert"]),
-            "clocks": clocks, "secondary": secondary,
+            "clocks": clocks, "multi_gpu": multi, "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     bf.close()
@@ -370,220 +414,206 @@ def main():
     return 0
 
 
-def secondary_3d(dev_index: int, world: int = 1, rank: int = 0, vols: int = 8):
-    """Volumes/s on C4b (3D 32x32 matrix probe, 64x64 lines, 4x4 multi-line,
-    pyramid scan conversion to 256^3, u8 line image and volume):
-      * "C4b_stream": ``vols`` volumes per call on every rank (C5's batched 3D
-        stream; one 1 GiB volume synthesised and replicated -- DAS cost is
-        data-independent), value = all ranks' volumes / max-over-ranks time;
-      * "C4b_single": ONE volume per call, latency mode: the
-        scanlines are split into event-aligned blocks over the ranks
-        (dist.ShardedVolume: DAS+envelope per block, all-reduce(max) of the
-        frame max, log compression, NCCL all-gather of the u8 line volume),
-        rank 0 scan-converts.  At N=1 it is the plain single-GPU call.
-    Device-timed with CUDA events, inputs resident in HBM (> L2)."""
-    import torch
-    import torch.distributed as dist
-    import synth
-    from synth import configs
-    from paper_1711_06127_b200 import SupraBF
-    from paper_1711_06127_b200.dist import ShardedVolume
-    out = {}
-    w = configs.CONFIGS["C4b"]().replace(sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
-    dev = torch.device(f"cuda:{dev_index}")
-    raw = torch.empty((vols, w.num_events, w.C, w.S), dtype=torch.int16, device=dev)
-    synth.channel_data_gpu(w, raw[0], realisation=0)
-    for v in range(1, vols):
-        raw[v].copy_(raw[0])
-    bf = SupraBF(w, device=dev_index, max_frames=vols)
-    li, img = bf.empty_line_img(vols), bf.empty_img(vols)
+# B200 unit counts for the ALU roofline (B200_PROFILING.md / the CUDA
+# throughput tables): 4 warp schedulers per SM each issue one warp
+# instruction per clock, 148 SMs, at the max SM clock.
+ISSUE_PEAK_WARP_INST_S = 148 * 4 * 1.965e9
 
-    def timed(fn, reps):
-        for _ in range(2):
-            fn()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
-            fn()
-        b.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t[0])
 
-    def stream_call():
-        bf.beamform(raw, vols, line_img=li)
-        bf.scanconvert(li, vols, img)
+def ncu_entry(key: str, frames: int):
+    """The committed ncu capture (profiles/das_ncu.json) of config ``key``'s
+    DAS launch at ``frames`` frames per call, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "das_ncu.json")) as f:
+            e = json.load(f).get(key, {})
+        return e if e.get("frames") == frames else None
+    except (OSError, ValueError):
+        return None
 
-    ms = timed(stream_call, 5)
-    out["C4b_stream"] = {"value": vols * world * 1000.0 / ms, "unit": "volumes/s", "ms_per_call": ms,
-                         "volumes_per_call_per_rank": vols, "scaling": "weak"}
 
-    sv = ShardedVolume(bf, w.L, w.S, torch.uint8, dev, align=4 * w.num_lines_x)
+def hbm_roofline(info: dict, frames: int, L: int, Sd: int, das_ms: float, key: str):
+    """DAS HBM roofline: algorithmic bytes = referenced int16 input (distinct
+    samples any tap reads, host-counted at create) + the f32 envelope written
+    (frame-max mode), per call, over the DAS launches' CUDA-event time."""
+    alg = (info["referenced_bytes_per_frame"] + L * Sd * 4) * frames
+    peak, kind = measured_peak_hbm()
+    ach = alg / (das_ms / 1000.0) / 1e9
+    e = ncu_entry(key, frames)
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": e.get("dram_bytes_per_launch") if e else None, "peak_kind": peak_kind_str(kind),
+            "das_ms_per_call": das_ms, "algorithmic_bytes_per_call": alg}
 
-    def single_call():
-        y = sv.run(raw[:1])
-        if rank == 0:
-            bf.scanconvert(y, 1, img)
 
-    ms = timed(single_call, 10)
-    out["C4b_single"] = {"value": 1000.0 / ms, "unit": "volumes/s", "ms_per_volume": ms,
-                         "volumes_per_call": 1, "scaling": "strong",
-                         "parallelism": f"scanline blocks x{world}, all-reduce(max) + all-gather u8 line volume"
-                         if world > 1 else "single GPU"}
-    bf.close()
-    del raw, li, img, sv
-    torch.cuda.empty_cache()
+def alu_roofline(info: dict, frames: int, das_ms: float, key: str):
+    """DAS ALU (issue) roofline for the multi-line shapes (M > 1: each input
+    sample feeds several lines, SURVEY 8(d) "ALU-bound"): warp instructions
+    the DAS launches issue per call (ncu smsp__inst_executed.sum of the same
+    launch shape, profiles/das_ncu.json) over their CUDA-event time, against
+    the issue peak 148 SMs x 4 schedulers x 1.965 GHz.  Also reported: taps/s
+    (taps = (line, sample, aperture member) triples per frame x frames)."""
+    taps = info["taps_per_frame"] * frames
+    out = {"bound": "alu", "unit": "warp-inst/s", "peak": ISSUE_PEAK_WARP_INST_S,
+           "peak_kind": "derived: 148 SMs x 4 issue/clk x 1.965 GHz (B200_PROFILING.md unit counts)",
+           "taps_per_s": taps / (das_ms / 1000.0), "das_ms_per_call": das_ms,
+           "hbm_frac": (info["referenced_bytes_per_frame"] * frames / (das_ms / 1000.0) / 1e9)
+           / measured_peak_hbm()[0]}
+    e = ncu_entry(key, frames)
+    if e and e.get("warp_inst_per_launch"):
+        ach = e["warp_inst_per_launch"] / (das_ms / 1000.0)
+        out.update({"achieved": ach, "frac": ach / ISSUE_PEAK_WARP_INST_S,
+                    "warp_inst_per_call": e["warp_inst_per_launch"],
+                    "inst_source": "profiles/das_ncu.json (ncu --set full)"})
+    else:
+        out.update({"achieved": None, "frac": None})
     return out
 
 
-def secondary_paper3d(dev_index: int, world: int = 1, rank: int = 0, vols: int = 4):
-    """Volumes/s on the paper's own 3D shape (C4p: 32x32 matrix probe through
-    384 channels, 32x16 scanlines, 60 deg, 70 mm, 0.175 mm pyramid output
-    401x401x402 u8): "C4p_single" one volume per
-    call, "C4p_stream" ``vols`` volumes per call per rank (weak scaling).
-    DAS + envelope/log + scan conversion, device-timed, inputs resident."""
+def peak_kind_str(kind: str) -> str:
+    return "measured (MEASURED_PEAKS.json hbm_gbs)" if kind == "measured" else kind
+
+
+def _timed_calls(bf, fn, reps: int, world: int, dev):
+    """(ms per call, DAS ms per call): CUDA events around the calls on the
+    current stream and the library's DAS events around each call's DAS
+    launches, after 2 warm-up calls; max over ranks."""
     import torch
     import torch.distributed as dist
-    import synth
-    from synth import configs
-    from paper_1711_06127_b200 import SupraBF
-    dev = torch.device(f"cuda:{dev_index}")
-    w = configs.c4p(sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
-    raw = torch.empty((vols, w.num_events, w.C, w.S), dtype=torch.int16, device=dev)
-    synth.channel_data_gpu(w, raw[0], realisation=0)
-    for v in range(1, vols):
-        raw[v].copy_(raw[0])
-    bf = SupraBF(w, device=dev_index, max_frames=vols)
-    li, img = bf.empty_line_img(vols), bf.empty_img(vols)
-    out = {}
-    for n, key, reps in ((1, "C4p_single", 10), (vols, "C4p_stream", 5)):
-        def call():
-            bf.beamform(raw, n, line_img=li)
-            bf.scanconvert(li, n, img)
-        for _ in range(2):
-            call()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
-            call()
-        b.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
-        out[key] = {"value": n * world * 1000.0 / ms, "unit": "volumes/s", "ms_per_call": ms,
-                    "volumes_per_call_per_rank": n, "scaling": "weak",
-                    "paper_gtx1080_vol_s_context": round(1000 / 27.49, 1)}
-    bf.close()
-    del raw, li, img
-    torch.cuda.empty_cache()
-    return out
-
-
-def secondary_sector(dev_index: int, world: int = 1, rank: int = 0, frames: int = 16):
-    """Frames/s on BASELINE.json configs[2] = C3: phased 128-element probe,
-    192 steered lines over 60 deg, 4096 samples, sector scan conversion to
-    512 x 512 u8; ``frames`` per call per rank (the config's 16-frame
-    batch), DAS + envelope/log + scan conversion, device-timed."""
-    import torch
-    import torch.distributed as dist
-    from synth import configs
-    from paper_1711_06127_b200 import SupraBF
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from gpu_util import raw_frames
-    dev = torch.device(f"cuda:{dev_index}")
-    w = configs.c3(sc_output_type=configs.T_U8)
-    raw = raw_frames(w, frames, device=dev)
-    bf = SupraBF(w, device=dev_index, max_frames=frames)
-    li, img = bf.empty_line_img(frames), bf.empty_img(frames)
-
-    def call():
-        bf.beamform(raw, frames, line_img=li)
-        bf.scanconvert(li, frames, img)
-    for _ in range(3):
-        call()
+    for _ in range(2):
+        fn()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    st = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for x, y in evs:
+        x.record(st)
+        y.record(st)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(10):
-        call()
-    b.record()
+    a.record(st)
+    for i in range(reps):
+        bf.set_das_events(*evs[i])
+        fn()
+    b.record(st)
     torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b) / 10], dtype=torch.float64, device=dev)
+    bf.set_das_events(None, None)
+    t = torch.tensor([a.elapsed_time(b) / reps, sum(x.elapsed_time(y) for x, y in evs) / reps],
+                     dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t[0])
+    return float(t[0]), float(t[1])
+
+
+def _volumes(w, n, dev, distinct=4):
+    """n frames/volumes on the device: realisations 0..distinct-1 (distinct
+    noise / speckle), cycled.  DAS cost does not depend on the data."""
+    import torch
+    import synth
+    out = torch.empty((n, w.num_events, w.C, w.S), dtype=torch.int16, device=dev)
+    k = max(1, min(n, distinct))
+    for v in range(k):
+        synth.channel_data_gpu(w, out[v], realisation=v)
+    for v in range(k, n):
+        out[v].copy_(out[v % k])
+    return out
+
+
+def secondary_line(key: str, w, n: int, reps: int, dev_index: int, world: int, unit: str, bound: str,
+                   extra=None):
+    """One device-timed secondary line: ``n`` frames/volumes per call on every
+    rank (weak scaling), DAS + envelope/log + scan conversion (u8 line image
+    and B-mode, frame-max reference), inputs resident in HBM; value = all
+    ranks' units / max-over-ranks time; roofline of the DAS launches."""
+    import torch
+    from paper_1711_06127_b200 import SupraBF
+    dev = torch.device(f"cuda:{dev_index}")
+    raw = _volumes(w, n, dev)
+    bf = SupraBF(w, device=dev_index, max_frames=n)
+    li, img = bf.empty_line_img(n), bf.empty_img(n)
+    info = bf.info()
+
+    def call():
+        bf.beamform(raw, n, line_img=li)
+        bf.scanconvert(li, n, img)
+    ms, das_ms = _timed_calls(bf, call, reps, world, dev)
+    Sd = w.S // max(1, w.decimation)
+    roof = (hbm_roofline(info, n, w.L, Sd, das_ms, key) if bound == "hbm"
+            else alu_roofline(info, n, das_ms, key))
+    out = {"value": n * world * 1000.0 / ms, "unit": unit, "ms_per_call": ms,
+           "per_call_per_rank": n, "scaling": "weak", "das_ms_per_call": das_ms,
+           "das_share": das_ms / ms, "frames_per_cta": info["frames_per_cta"], "roofline": roof,
+           "input_gib_per_call": round(n * w.raw_bytes_per_frame() / 2 ** 30, 3)}
+    if extra:
+        out.update(extra)
     bf.close()
     del raw, li, img
     torch.cuda.empty_cache()
-    return {"C3": {"value": frames * world * 1000.0 / ms, "unit": "frames/s", "ms_per_call": ms,
-                   "frames_per_call_per_rank": frames, "scaling": "weak"}}
+    return out
+
+
+def secondary_all(dev_index: int, world: int, rank: int):
+    from synth import configs
+    u8 = dict(sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
+    ctx3d = {"paper_gtx1080_vol_s_context": round(1000 / 27.49, 1)}
+    out = {}
+    # 3D, 32x32 matrix probe, 64x64 lines, 2048 samples, pyramid 256^3
+    out["C4a_single"] = secondary_line("C4a", configs.c4("a", **u8), 1, 5, dev_index, world, "volumes/s",
+                                       "hbm", {"lines": 4096, "events": 4096,
+                                               "note": "M = 1: 16 GiB of int16 per volume, HBM-bound"})
+    out["C4b_stream"] = secondary_line("C4b", configs.c4("b", **u8), 8, 5, dev_index, world, "volumes/s",
+                                       "alu", {"note": "4x4 multi-line (each sample feeds 16 lines): ALU-bound"})
+    out["C4b_single"] = secondary_c4b_single(dev_index, world, rank)
+    # the paper's 3D row: 384 channels, 32x16 lines, 70 mm, 401x401x402
+    out["C4p_single"] = secondary_line("C4p", configs.c4p(**u8), 1, 10, dev_index, world, "volumes/s",
+                                       "hbm", ctx3d)
+    out["C4p_stream"] = secondary_line("C4p", configs.c4p(**u8), 4, 5, dev_index, world, "volumes/s",
+                                       "hbm", ctx3d)
+    # BASELINE configs[2]: phased 128 el, 192 lines, 4096 samples, sector 512^2
+    out["C3"] = secondary_line("C3", configs.c3(sc_output_type=configs.T_U8), 16, 10, dev_index, world,
+                               "frames/s", "hbm")
+    for name, fps in PAPER_T1_GTX1080_FPS.items():
+        out[name] = secondary_line(name, configs.CONFIGS[name](**u8), 64, 10, dev_index, world, "frames/s",
+                                   "hbm" if name.endswith("_1") else "alu",
+                                   {"paper_gtx1080_fps_context": round(fps, 1)})
+    return out
+
+
+def secondary_c4b_single(dev_index: int, world: int, rank: int):
+    """ONE C4b volume per call, latency mode: the scanlines
+    are split into event-aligned blocks over the ranks (dist.ShardedVolume:
+    DAS+envelope per block, all-reduce(max) of the frame max, log
+    compression, NCCL all-gather of the u8 line volume), rank 0
+    scan-converts.  At N=1 it is the single-GPU call."""
+    import torch
+    from synth import configs
+    from paper_1711_06127_b200 import SupraBF
+    from paper_1711_06127_b200.dist import ShardedVolume
+    w = configs.c4("b", sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
+    dev = torch.device(f"cuda:{dev_index}")
+    raw = _volumes(w, 1, dev)
+    bf = SupraBF(w, device=dev_index, max_frames=1)
+    img = bf.empty_img(1)
+    info = bf.info()
+    sv = ShardedVolume(bf, w.L, w.S, torch.uint8, dev, align=4 * w.num_lines_x)
+
+    def call():
+        y = sv.run(raw)
+        if rank == 0:
+            bf.scanconvert(y, 1, img)
+    ms, das_ms = _timed_calls(bf, call, 10, world, dev)
+    out = {"value": 1000.0 / ms, "unit": "volumes/s", "ms_per_volume": ms, "volumes_per_call": 1,
+           "scaling": "strong", "das_ms_per_call": das_ms, "roofline": alu_roofline(info, 1, das_ms, "C4b_1"),
+           "parallelism": f"scanline blocks x{world}, all-reduce(max) + all-gather u8 line volume"
+           if world > 1 else "single GPU"}
+    bf.close()
+    del raw, img, sv
+    torch.cuda.empty_cache()
+    return out
 
 
 # The paper's own 2D benchmark rows (Table 1, P:329-332): GeForce GTX 1080
 # total node run-time per frame -> frames/s, quoted as context only.
 PAPER_T1_GTX1080_FPS = {"T1_64_1": 1000 / 5.37, "T1_64_2": 1000 / 4.24, "T1_128_1": 1000 / 4.38,
                         "T1_128_2": 1000 / 5.00}
-
-
-def secondary_table1(dev_index: int, world: int = 1, rank: int = 0, frames: int = 64):
-    """Frames/s on the paper's Table-1 2D shapes:
-    128-element linear probe with 64 receive channels (walking aperture),
-    (transmit events / multi-line) = 64/1, 64/2, 128/1, 128/2, 45 mm depth,
-    u8 B-mode on the 0.0225 mm grid.  ``frames`` per call on every rank
-    (weak scaling), DAS + envelope/log + scan conversion, device-timed with
-    CUDA events, inputs resident in HBM."""
-    import torch
-    import torch.distributed as dist
-    from synth import configs
-    from paper_1711_06127_b200 import SupraBF
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from gpu_util import raw_frames
-    dev = torch.device(f"cuda:{dev_index}")
-    out = {}
-    for name, paper_fps in PAPER_T1_GTX1080_FPS.items():
-        w = configs.CONFIGS[name](sc_output_type=configs.T_U8, line_output_type=configs.T_U8)
-        raw = raw_frames(w, frames, device=dev)
-        bf = SupraBF(w, device=dev_index, max_frames=frames)
-        li, img = bf.empty_line_img(frames), bf.empty_img(frames)
-
-        def call():
-            bf.beamform(raw, frames, line_img=li)
-            bf.scanconvert(li, frames, img)
-        for _ in range(3):
-            call()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 10
-        a.record()
-        for _ in range(reps):
-            call()
-        b.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
-        out[name] = {"value": frames * world * 1000.0 / ms, "unit": "frames/s", "ms_per_call": ms,
-                     "frames_per_call_per_rank": frames, "lines": w.L, "channels": w.C,
-                     "scaling": "weak", "paper_gtx1080_fps_context": round(paper_fps, 1)}
-        bf.close()
-        del raw, li, img
-        torch.cuda.empty_cache()
-    return out
 
 
 if __name__ == "__main__":

@@ -18,8 +18,21 @@
  * ---------------------------------------
  *  * All data buffers are CALLER-OWNED device memory on cfg.device,
  *    contiguous, in the layouts stated below.  The library never frees or
- *    retains them beyond the call and never allocates per call, so every call
- *    is capturable in a CUDA graph.
+ *    retains them beyond the call and never allocates device or pinned memory
+ *    per call, never synchronises the host with a stream, and passes every
+ *    per-call tensor map by value as a kernel parameter -- so every call is
+ *    capturable in a CUDA graph (a captured graph keeps its own copy of the
+ *    parameters; tests/test_graph_gpu.py replays one over rotating buffers).
+ *    Per (raw buffer, frames) the host encodes S/32 tensor maps once and
+ *    keeps them in a small host-side cache (8 entries); a miss costs host
+ *    time only.
+ *  * Results are deterministic.  For every call with frames >= 2 the RF and
+ *    line image of a frame are bitwise independent of the batch it is in
+ *    (its position, the batch size, the launch shape: one summation order
+ *    per configuration).  A call with frames = 1 and samples in
+ *    {1024, 2048} uses a single-frame kernel that splits the aperture over
+ *    warps; it agrees with the batched result to float32 rounding
+ *    (normwise RF difference <= 1e-6).
  *  * Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL
  *    = legacy default stream).  Validation errors are returned synchronously
  *    before anything is enqueued.  A device fault raised by an earlier launch
@@ -69,7 +82,9 @@ enum { SUPRA_SC_LINEAR_2D = 0, SUPRA_SC_SECTOR_2D = 1, SUPRA_SC_PYRAMID_3D = 2 }
  *   samples held in registers per thread); input_type = SUPRA_T_I16;
  *   sample_frequency > 0; speed_of_sound in [1000, 2000];
  *   f_number > 0; window, normalize in their enums;
- *   fir_taps odd, 1..129; decimation = 1 (>1 is future work);
+ *   fir_taps odd, 1..129; decimation d >= 1 with samples_per_channel / d
+ *   >= 2 (the line image keeps k = d q, q < samples / d, and scan
+ *   conversion treats it as samples/d samples spaced d dr);
  *   0 < demod_frequency - bw/2 and demod_frequency + bw/2 < fs/2 (S:188,
  *   S:196); dynamic_range_db > 0; reference_value > 0 when
  *   reference_mode = FIXED; spacing > 0 and out_dims >= 1;
@@ -177,11 +192,13 @@ supra_status supra_bf_create(const supra_bf_config *cfg, supra_bf_t *out);
  * Arguments:
  *   raw      : device, int16 [frames][num_events][channels][samples], 16-byte aligned
  *              (channels = num_channels, or Nx*Ny when num_channels = 0)
- *              (read through a TMA tensor map encoded per call).
+ *              (read through TMA tensor maps encoded on the host per
+ *              (buffer, frames), cached, and passed as kernel parameters).
  *   frames   : 0 .. max_frames_per_call (0 = no-op).
  *   rf       : device float [frames][L][samples] or NULL.
- *   line_img : device [frames][L][samples] of line_output_type or NULL
- *              (non-NULL runs the fused envelope + log epilogue).
+ *   line_img : device [frames][L][samples / decimation] of line_output_type
+ *              or NULL (non-NULL runs the fused envelope + log epilogue).
+ *              RF keeps all samples; the line image keeps k = d q.
  *   stream   : cudaStream_t.
  * Errors: SUPRA_E_STRUCT if both outputs are NULL, raw is NULL/misaligned,
  * frames out of range, or a pointer is not device memory of cfg.device.
@@ -193,7 +210,7 @@ supra_status supra_bf_beamform(supra_bf_t h, const void *raw, int32_t frames, fl
  * supra_bf_envelope_log -- the unfused epilogue on an RF buffer: IQ envelope
  * + log compression exactly as above, for `frames` frames.
  *   rf       : device float [frames][L][samples].
- *   line_img : device [frames][L][samples] of line_output_type.
+ *   line_img : device [frames][L][samples / decimation] of line_output_type.
  * Errors: SUPRA_E_STRUCT on NULL / frames out of range.
  */
 supra_status supra_bf_envelope_log(supra_bf_t h, const float *rf, int32_t frames, void *line_img,
@@ -208,7 +225,7 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float *rf, int32_t frames
  * supra_bf_beamform_lines -- DAS + IQ envelope (the formulas of
  * supra_bf_beamform, without the log step) for lines
  * [line_first, line_first + line_count) of every frame.
- *   env       : device float [frames][L][samples]; only the range's rows are
+ *   env       : device float [frames][L][samples / decimation]; only the range's rows are
  *               written (envelope, >= 0).
  *   frame_max : device float [frames]; receives the maximum of env over the
  *               range (0 for an all-zero range) -- all-reduce(max) it across
@@ -220,7 +237,7 @@ supra_status supra_bf_envelope_log(supra_bf_t h, const float *rf, int32_t frames
  * (0 where env = 0 or ref = 0) on the same line range; ref =
  * frame_max[f] (device float [frames]) in SUPRA_REF_FRAME_MAX mode,
  * reference_value in SUPRA_REF_FIXED mode (frame_max may then be NULL).
- *   line_img  : device [frames][L][samples] of line_output_type; only the
+ *   line_img  : device [frames][L][samples / decimation] of line_output_type; only the
  *               range's rows are written.  env and line_img may alias only
  *               when line_output_type is SUPRA_T_F32 (element-wise, in place).
  * Errors: SUPRA_E_STRUCT on NULL (frame_max NULL in FRAME_MAX mode), a range
@@ -238,7 +255,7 @@ supra_status supra_bf_log_compress(supra_bf_t h, const float *env, int32_t frame
  * indices (built in binary64, bit-exact with the analytic inverse map) and
  * fractions; the log-compressed line image is blended bilinearly (2D) or
  * trilinearly (3D) (reading #23).  Invalid pixels are 0 with mask 0.
- *   line_img : device [frames][Ly][Lx][samples] of line_output_type.
+ *   line_img : device [frames][Ly][Lx][samples / decimation] of line_output_type.
  *   img      : device [frames][nz][ny][nx] of sc_output_type (x fastest).
  *   mask     : device uint8 [nz][ny][nx] or NULL (frame-independent).
  * Errors: SUPRA_E_STRUCT on NULL / frames out of range.
@@ -277,7 +294,8 @@ const char *supra_bf_last_error(void);
  * supra_bf_sc_indices -- copy the scan-conversion table's integer part to
  * host memory for bit-exact comparison with an independent inverse map:
  * for every output pixel n (x fastest): valid[n] in {0,1} and
- * idx[3n..3n+2] = (i0x, i0y, k0) as int32 (undefined where valid = 0).
+ * idx[3n..3n+2] = (i0x, i0y, k0) as int32 (undefined where valid = 0);
+ * k0 indexes the (decimated) line image, samples / decimation long.
  *   valid : host uint8 [nz*ny*nx];  idx : host int32 [nz*ny*nx][3].
  * Synchronous.  Errors: SUPRA_E_STRUCT on NULL.
  */

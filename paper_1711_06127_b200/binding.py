@@ -14,9 +14,9 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# SUPRA_BF_LIB: dev-only override with another build of the same library
-# (A/B measurements of kernel variants); the default is the in-tree build.
-LIB_PATH = os.environ.get("SUPRA_BF_LIB") or os.path.join(HERE, "libsupra_bf.so")
+# The in-tree build.  No environment variable selects another library: a
+# dev script that A/B-times a variant build calls use_library() explicitly.
+LIB_PATH = os.path.join(HERE, "libsupra_bf.so")
 
 ABI_VERSION = 2
 MAX_BANDS = 4
@@ -110,6 +110,15 @@ def lib():
         L.supra_bf_beamform_bmode.restype = C.c_int
         _lib = L
     return _lib
+
+
+def use_library(path: str):
+    """Dev aid (scripts/ only): load another build of the same library, e.g.
+    _variants/<name>/libsupra_bf.so, before the first handle is created."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("the library is already loaded")
+    LIB_PATH = path
 
 
 def _check(rc: int):

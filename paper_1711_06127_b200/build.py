@@ -35,7 +35,7 @@ def _stale(out, deps):
 def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, variant: str = "",
           defines=()) -> str:
     """Build the library; ``variant``/``defines`` build an A/B variant into
-    _variants/<variant>/libsupra_bf.so (dev aid, selected with SUPRA_BF_LIB)."""
+    _variants/<variant>/libsupra_bf.so (dev aid, loaded with binding.use_library)."""
     global BUILD, OUT
     if variant:
         BUILD = os.path.join(ROOT, "_variants", variant, "_build")

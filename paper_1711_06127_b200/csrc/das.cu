@@ -7,30 +7,30 @@
 
 namespace supra {
 
-extern template cudaError_t launch_k<16, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<16, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<8, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<8, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<8, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<8, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<4, 16, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<4, 16, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<4, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<4, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<4, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<4, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<2, 16, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<2, 16, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<2, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<2, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<2, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<2, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<1, 16, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<1, 16, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<1, 8, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<1, 8, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<1, 4, false>(const CUtensorMap&, const DasArgs&, cudaStream_t);
-extern template cudaError_t launch_k<1, 4, true>(const CUtensorMap&, const DasArgs&, cudaStream_t);
+extern template cudaError_t launch_k<16, 4, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<16, 4, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<8, 8, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<8, 8, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<8, 4, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<8, 4, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<4, 16, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<4, 16, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<4, 8, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<4, 8, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<4, 4, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<4, 4, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<2, 16, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<2, 16, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<2, 8, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<2, 8, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<2, 4, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<2, 4, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 16, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 16, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 8, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 8, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 4, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 4, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 
 size_t das_smem_bytes(int FB, int NT, int nent_max, int fir_taps) {
   return das_smem_bytes_impl(FB, NT, nent_max, fir_taps);
@@ -45,9 +45,11 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps) {
                                 {2, 8},  {2, 4}, {1, 16}, {1, 8}, {1, 4}};
   const int ntmax = das_nt(S);
   const int P = (fir_taps - 1) / 2;
-  // dev override (A/B measurements): SUPRA_BF_SHAPE=<fb>x<nt>
   int ofb = 0, ont = 0;
+#ifdef SUPRA_DEV_KNOBS
+  // dev override (A/B measurements only): SUPRA_BF_SHAPE=<fb>x<nt>
   if (const char* ev = std::getenv("SUPRA_BF_SHAPE")) std::sscanf(ev, "%dx%d", &ofb, &ont);
+#endif
   for (int ci = -1; ci < (int)(sizeof cand / sizeof cand[0]); ci++) {
     const int fb = ci < 0 ? ofb : cand[ci][0], nt = ci < 0 ? ont : cand[ci][1];
     if (ci < 0 && !((fb == 16 && nt == 4) || (fb == 8 && (nt == 4 || nt == 8)))) continue;
@@ -62,26 +64,32 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps) {
 }
 
 template <bool T0>
-static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, DasShape sh, cudaStream_t st) {
+static cudaError_t launch_t0(const CUtensorMap& tm, const DasArgs& a, const RawMaps& m, DasShape sh,
+                             cudaStream_t st) {
   const int nt = sh.nt;
   switch (sh.fb) {
-    case 16: return launch_k<16, 4, T0>(tm, a, st);
-    case 8: return nt == 4 ? launch_k<8, 4, T0>(tm, a, st) : launch_k<8, 8, T0>(tm, a, st);
+    case 16: return launch_k<16, 4, T0>(tm, a, m, st);
+    case 8: return nt == 4 ? launch_k<8, 4, T0>(tm, a, m, st) : launch_k<8, 8, T0>(tm, a, m, st);
     case 4:
-      return nt == 4 ? launch_k<4, 4, T0>(tm, a, st)
-                     : (nt == 8 ? launch_k<4, 8, T0>(tm, a, st) : launch_k<4, 16, T0>(tm, a, st));
+      return nt == 4 ? launch_k<4, 4, T0>(tm, a, m, st)
+                     : (nt == 8 ? launch_k<4, 8, T0>(tm, a, m, st) : launch_k<4, 16, T0>(tm, a, m, st));
     case 2:
-      return nt == 4 ? launch_k<2, 4, T0>(tm, a, st)
-                     : (nt == 8 ? launch_k<2, 8, T0>(tm, a, st) : launch_k<2, 16, T0>(tm, a, st));
+      return nt == 4 ? launch_k<2, 4, T0>(tm, a, m, st)
+                     : (nt == 8 ? launch_k<2, 8, T0>(tm, a, m, st) : launch_k<2, 16, T0>(tm, a, m, st));
     default:
-      return nt == 4 ? launch_k<1, 4, T0>(tm, a, st)
-                     : (nt == 8 ? launch_k<1, 8, T0>(tm, a, st) : launch_k<1, 16, T0>(tm, a, st));
+      return nt == 4 ? launch_k<1, 4, T0>(tm, a, m, st)
+                     : (nt == 8 ? launch_k<1, 8, T0>(tm, a, m, st) : launch_k<1, 16, T0>(tm, a, m, st));
   }
 }
 
-cudaError_t launch_das(const CUtensorMap& tm, const DasArgs& a, DasShape sh, cudaStream_t st) {
-  if (das_warp_ok(sh.fb, a.S, a.t0fs) && !std::getenv("SUPRA_BF_NO_WARP")) return launch_das_warp(tm, a, st);
-  return a.t0fs != 0.f ? launch_t0<true>(tm, a, sh, st) : launch_t0<false>(tm, a, sh, st);
+cudaError_t launch_das(const CUtensorMap& tm, const DasArgs& a, const RawMaps& m, DasShape sh, bool allow_warp,
+                       cudaStream_t st) {
+  bool warp = allow_warp && das_warp_ok(sh.fb, a.S, a.t0fs);
+#ifdef SUPRA_DEV_KNOBS
+  if (std::getenv("SUPRA_BF_NO_WARP")) warp = false;  // A/B measurements only
+#endif
+  if (warp) return launch_das_warp(tm, a, st);
+  return a.t0fs != 0.f ? launch_t0<true>(tm, a, m, sh, st) : launch_t0<false>(tm, a, m, sh, st);
 }
 
 }  // namespace supra

@@ -163,20 +163,23 @@ __device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4
                                            uint32_t sbase, int kt, int k0, float kt0f) {
   const int k = k0 + m * kTileK + kt;
   const bool mem = !(m < M0 + tile_gran(NT)) || k >= kenter;
-  const float kf = kt0f + (float)(m * kTileK);
-  const float h = 0.5f * kf;
-  const float h2 = (m == 0 && k == 0) ? 1e-20f : h * h;  // r2 > 0 even at k = 0, q = 0
+  const float kf = __fadd_rn(kt0f, (float)(m * kTileK));
+  const float h = __fmul_rn(0.5f, kf);
+  const float h2 = (m == 0 && k == 0) ? 1e-20f : __fmul_rn(h, h);  // r2 > 0 even at k = 0, q = 0
   float delta = split_delay(r.x, r.y, h, h2);
-  if (T0) delta += a.t0fs;
+  if (T0) delta = __fadd_rn(delta, a.t0fs);
   const float tf = __fadd_rd(delta, kFloorMagic);
   // &x[i0] - 512 m = sbase + 2 (i0 - ws) - 512 m = 2 bits(tf) + (sbase - 2 wsm)  (wsm = ws + magic - k0 - kt)
   const uint32_t ad = 2u * (uint32_t)__float_as_int(tf) + (sbase - 2u * (uint32_t)wsm);
-  const float fr = (delta - (tf - kFloorMagic)) * a.fr_scale;
-  float w = fmaf(__cosf(r.z * rcp_ftz(fmaxf(kf, 1.f))), a.win_b, a.win_a);
+  // explicit _rn intrinsics: no FMA contraction, so each lane computes
+  // exactly what tile_geo2's packed operations compute (bitwise equality
+  // across launch shapes, where a tile is computed alone or in a pair)
+  const float fr = __fmul_rn(__fsub_rn(delta, __fsub_rn(tf, kFloorMagic)), a.fr_scale);
+  float w = fmaf(__cosf(__fmul_rn(r.z, rcp_ftz(fmaxf(kf, 1.f)))), a.win_b, a.win_a);
   w = mem ? w : 0.f;
   // linear interpolation as two weights: w (1-f) x[i0] + w f x[i0+1]
-  const float w1 = w * fr;
-  return TapGeo{mem ? ad : sbase - 2u * (uint32_t)(m * kTileK), w - w1, w1};
+  const float w1 = __fmul_rn(w, fr);
+  return TapGeo{mem ? ad : sbase - 2u * (uint32_t)(m * kTileK), __fsub_rn(w, w1), w1};
 }
 
 // Geometry of tiles m, m+1 together in packed f32x2 (FFMA2 / FADD2.RM /
@@ -267,7 +270,8 @@ __device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const fl
 
 template <int FB, int NT, bool T0>
 __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                          const DasArgs a) {
+                                                          const DasArgs a,
+                                                          const __grid_constant__ RawMaps rmaps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int PL = NT * kTileK;                 // samples per pass
   constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
@@ -297,8 +301,8 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
-  if (a.raw_maps && (int)threadIdx.x < S / kRowSamples)
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.raw_maps + threadIdx.x))
+  if (a.row_cut && (int)threadIdx.x < S / kRowSamples)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmaps.m[threadIdx.x]))
                  : "memory");
   if (threadIdx.x < 16) sm.smax[threadIdx.x] = 0u;
 
@@ -322,16 +326,30 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       const int i = i0 + threadIdx.x;
       np += __syncthreads_count(i < nent && ents[i].kenter < kend);
     }
-    // Entry records of the pass, in device order: alternate the long-trace
-    // (early k_enter) and short-trace ends of the prefix so consecutive
-    // ring entries carry similar work.  Window [ws, ws + rows*32),
-    // rows = PL/32 + 2, ws <= floor(tau(kb)) - 2 and 32-aligned, kb =
-    // max(k_enter, k0): d tau/dk in [0, 1] keeps i0(k) + 1 inside the
-    // window for every member k of the pass; reads outside the record come
-    // back as TMA zeros.  (The sum order is fixed per configuration: results
-    // are deterministic and identical across frames and batch sizes.)
+    // Entry records of the pass, in device order.  The order is ONE global
+    // sequence per line group -- the k_enter-sorted list taken alternately
+    // from its long-trace (early k_enter) and short-trace ends, so
+    // consecutive ring entries carry similar work -- filtered to the pass's
+    // prefix (entries [0, np)).  Filtering keeps the relative order, so the
+    // members of any output sample k are summed in the same order whatever
+    // the pass boundaries (NT), frame grouping (FB) or batch size: the RF of
+    // a frame is bitwise independent of the call it is beamformed in
+    // (S:164).  Non-members inside a pass add an exact +0.  The i-th record
+    // of the filtered sequence, with h = nent - np entries outside the pass:
+    // i < h -> entry i; else t = i - h, j = h + t/2, entry j (t even) or
+    // nent - 1 - j (t odd).
+    // Window [ws, ws + rows*32), rows = PL/32 + 2, ws <= floor(tau(kb)) - 2
+    // and 32-aligned, kb = max(k_enter, k0): d tau/dk in [0, 1] keeps
+    // i0(k) + 1 inside the window for every member k of the pass; reads
+    // outside the record come back as TMA zeros.
+    const int hcut = nent - np;
     for (int i = threadIdx.x; i < np; i += blockDim.x) {
-      const DasEntry e = ents[(i & 1) ? np - 1 - i / 2 : i / 2];
+      int ei = i;
+      if (i >= hcut) {
+        const int t = i - hcut, jj = hcut + (t >> 1);
+        ei = (t & 1) ? nent - 1 - jj : jj;
+      }
+      const DasEntry e = ents[ei];
       const float B = fmaf(dir.z, e.qz, fmaf(dir.y, e.qy, dir.x * e.qx));
       const float Ah = 0.5f * e.A;
       const int kb = max(e.kenter, k0);
@@ -352,9 +370,9 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
     // TMA of entry jj's window (all FB frames) into ring slot `buf`.
     auto produce = [&](int jj, int buf) {
       const int2 we = sm.wse[jj];
-      // rows at or past rcut are out of bounds in raw_maps[rcut - 1]: zero
+      // rows at or past rcut are out of bounds in rmaps.m[rcut - 1]: zero
       // fill, no DRAM read (the box size, and so the tx count, is fixed)
-      const CUtensorMap* m = a.raw_maps ? a.raw_maps + ((we.y >> 20) - 1) : &tmap;
+      const CUtensorMap* m = a.row_cut ? &rmaps.m[(we.y >> 20) - 1] : &tmap;
       mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
       tma_load_5d((unsigned char*)sm.stage + buf * SB, m, 0, we.x / kRowSamples, we.y & 0xFFFFF, ev, fm,
                   &sm.full[buf]);
@@ -494,7 +512,7 @@ inline size_t das_smem_bytes_impl(int FB, int NT, int nent_max, int fir_taps) {
 }
 
 template <int FB, int NT, bool T0>
-cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
+cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, const RawMaps& maps, cudaStream_t st) {
   const size_t smem = das_smem_bytes_impl(FB, NT, a.entries_per_group, a.fir_taps);
   auto kern = das_fused_kernel<FB, NT, T0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -509,7 +527,7 @@ cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = a.pdl_wait_end ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, tm, a);
+  return cudaLaunchKernelEx(&cfg, kern, tm, a, maps);
 }
 
 }  // namespace supra

@@ -296,7 +296,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     v[m] = s * inv;
     if (a.rf) a.rf[((size_t)f0 * a.L + line) * S + k] = v[m];
   }
-  if (!a.do_epilogue) return;
+  if (!a.do_epilogue) {
+    // a PDL secondary still retires only after the primary grid
+    if (a.pdl_wait_end) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   __syncthreads();  // partials read: the ring becomes the FIR line buffer
   float4* lineb = (float4*)ring;
   const int kbase = -2 * P;

@@ -89,16 +89,20 @@ struct supra_bf {
   float band_w[kMaxBands] = {1.f, 0.f, 0.f, 0.f};
   std::vector<float> fir_c, fir_s;  // [kMaxBands][kMaxHalfTaps + 1]
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
-  // per-(raw buffer, frames, shape) sets of row-cut tensor maps (DasArgs::
-  // raw_maps), encoded once and kept on the device; small LRU
+  // per-(raw buffer, frames, shape) row-cut tensor-map sets, HOST memory
+  // only: each launch passes its set by value as a kernel parameter, so a
+  // set can be re-encoded at any time without synchronisation (LRU of
+  // kMapCache entries; a miss costs S/32 host encodes, never a device
+  // allocation or a stall)
+  static constexpr int kMapCache = 8;
   struct MapSet {
     const void* raw = nullptr;
     int F = 0, fb = 0, nt = 0;
-    CUtensorMap* d = nullptr;  // device [S/32]
-    CUtensorMap* h = nullptr;  // pinned host staging
+    uint64_t used = 0;
+    RawMaps maps;
   };
-  MapSet mcache[4];
-  int mnext = 0;
+  std::vector<MapSet> mcache;
+  uint64_t mclock = 0;
   int64_t info[8] = {0};
 };
 
@@ -118,11 +122,7 @@ void free_all(supra_bf* h) {
                   h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_blk_kmin, h->d_col_l0, h->d_col_nl, h->d_rows, h->d_ent};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  for (auto& m : h->mcache) {
-    if (m.d) cudaFree(m.d);
-    if (m.h) cudaFreeHost(m.h);
-    m = supra_bf::MapSet{};
-  }
+  h->mcache.clear();
 }
 
 // Element (i,j) position, S:30 (same definition the oracle writes out).
@@ -636,41 +636,33 @@ bool make_raw_map(CUtensorMap* m, const void* raw, int F, int E, int C, int S, i
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Row-cut map set for DasArgs::raw_maps: m[r-1] = make_raw_map with only r
-// time rows in range.  Cached per (raw, F, fb, nt); NULL on failure (the
-// kernel then uses its single map).
-const CUtensorMap* row_cut_maps(supra_bf* h, const void* raw, int F, int fb, int nt, cudaStream_t st) {
-  for (auto& m : h->mcache)
-    if (m.d && m.raw == raw && m.F == F && m.fb == fb && m.nt == nt) return m.d;
+// Row-cut map set (RawMaps, a kernel parameter): m[r-1] = make_raw_map with
+// only r time rows in range.  Cached on the host per (raw, F, fb, nt); NULL
+// on failure (the kernel then uses its single map).
+const RawMaps* row_cut_maps(supra_bf* h, const void* raw, int F, int fb, int nt) {
+  h->mclock++;
+  supra_bf::MapSet* victim = nullptr;
+  for (auto& m : h->mcache) {
+    if (m.raw == raw && m.F == F && m.fb == fb && m.nt == nt) {
+      m.used = h->mclock;
+      return &m.maps;
+    }
+    if (!victim || m.used < victim->used) victim = &m;
+  }
+  if ((int)h->mcache.size() < supra_bf::kMapCache) {
+    h->mcache.emplace_back();
+    victim = &h->mcache.back();
+  }
+  victim->raw = nullptr;
   const int R = h->S / kRowSamples;
-  auto& m = h->mcache[h->mnext];
-  h->mnext = (h->mnext + 1) % 4;
-  if (!m.d && cudaMalloc((void**)&m.d, sizeof(CUtensorMap) * (kMaxSamples / kRowSamples)) != cudaSuccess) {
-    cudaGetLastError();
-    m.d = nullptr;
-    return nullptr;
-  }
-  if (!m.h && cudaMallocHost((void**)&m.h, sizeof(CUtensorMap) * (kMaxSamples / kRowSamples)) != cudaSuccess) {
-    cudaGetLastError();
-    m.h = nullptr;
-    return nullptr;
-  }
-  // an evicted slot's previous upload may still be pending on the stream
-  if (m.raw) cudaStreamSynchronize(st);
-  m.raw = nullptr;
   for (int r = 1; r <= R; r++)
-    if (!make_raw_map(&m.h[r - 1], raw, F, h->E, h->C, h->S, das_rows_nt(nt), fb, r)) return nullptr;
-  // ordered before the kernel on the same stream; the staging buffer is not
-  // rewritten while this entry stays cached
-  if (cudaMemcpyAsync(m.d, m.h, sizeof(CUtensorMap) * R, cudaMemcpyHostToDevice, st) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  m.raw = raw;
-  m.F = F;
-  m.fb = fb;
-  m.nt = nt;
-  return m.d;
+    if (!make_raw_map(&victim->maps.m[r - 1], raw, F, h->E, h->C, h->S, das_rows_nt(nt), fb, r)) return nullptr;
+  victim->raw = raw;
+  victim->F = F;
+  victim->fb = fb;
+  victim->nt = nt;
+  victim->used = h->mclock;
+  return &victim->maps;
 }
 
 bool is_device_ptr(const void* p, int dev) {
@@ -739,10 +731,13 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   // DAS launch shape
   const int maxF = cfg->max_frames_per_call;
   h->frames_per_cta = 16;  // upper bound; das_shape() picks per call
-  if (const char* ev = std::getenv("SUPRA_BF_FRAMES_PER_CTA")) {
+#ifdef SUPRA_DEV_KNOBS
+  if (const char* ev = std::getenv("SUPRA_BF_FRAMES_PER_CTA")) {  // A/B measurements only
     int v = std::atoi(ev);
     if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) h->frames_per_cta = v;
   }
+#endif
+  h->mcache.reserve(supra_bf::kMapCache);  // entries never move (launches point into them)
   const DasShape sh = das_shape(h->frames_per_cta, h->S, maxF, h->entries_per_group, cfg->fir_taps);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
   // f32 line-domain scratch [maxF][L][S/dec]: the envelope of a frame-max
@@ -877,20 +872,28 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.pdl_wait_end = 0;
   // exact trace windows for the multi-pass / multi-frame kernel (the
   // single-frame kernel's windows run to the end of the record anyway)
-  const bool exact = !std::getenv("SUPRA_BF_NO_ROWCUT");
-  a.raw_maps = (exact && !das_warp_ok(sh.fb, h->S, a.t0fs)) ? row_cut_maps(h, raw, Fmain, sh.fb, sh.nt, st) : nullptr;
+  bool exact = true;
+#ifdef SUPRA_DEV_KNOBS
+  if (std::getenv("SUPRA_BF_NO_ROWCUT")) exact = false;  // A/B measurements only
+#endif
+  // the warp-split kernel only for a single-frame call; remainders of a
+  // multi-frame call use das_fused_kernel (batch-independent results)
+  const bool warp1 = frames == 1 && das_warp_ok(sh.fb, h->S, a.t0fs);
+  static const RawMaps kNoMaps{};
+  const RawMaps* m1 = (exact && !warp1) ? row_cut_maps(h, raw, Fmain, sh.fb, sh.nt) : nullptr;
+  a.row_cut = m1 != nullptr;
   if (h->ev_before) cudaEventRecord(h->ev_before, st);
-  supra_status s = check_launch(launch_das(tm, a, sh, st), "das kernel");
+  supra_status s = check_launch(launch_das(tm, a, m1 ? *m1 : kNoMaps, sh, frames == 1, st), "das kernel");
   if (s == SUPRA_OK && rem) {
     DasArgs a2 = a;
     a2.fbase = Fmain;
     a2.Fmap = rem;
     a2.pdl_trigger = 0;
     a2.pdl_wait_end = 1;
-    a2.raw_maps = (exact && !das_warp_ok(sh2.fb, h->S, a.t0fs))
-                      ? row_cut_maps(h, (const char*)raw + Fmain * frame_bytes, rem, sh2.fb, sh2.nt, st)
-                      : nullptr;
-    s = check_launch(launch_das(tm2, a2, sh2, st), "das kernel (remainder frames)");
+    const RawMaps* m2 = exact ? row_cut_maps(h, (const char*)raw + Fmain * frame_bytes, rem, sh2.fb, sh2.nt)
+                              : nullptr;
+    a2.row_cut = m2 != nullptr;
+    s = check_launch(launch_das(tm2, a2, m2 ? *m2 : kNoMaps, sh2, false, st), "das kernel (remainder frames)");
   }
   if (h->ev_after) cudaEventRecord(h->ev_after, st);
   if (s != SUPRA_OK || !line_img || a.ref_fixed || env_ext) return s;
@@ -1138,7 +1141,9 @@ supra_status supra_bf_beamform_bmode(supra_bf_t h, const void* raw, int32_t fram
 supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t* valid, int32_t* idx) {
   if (!h || !valid || !idx) return fail(SUPRA_E_STRUCT, "NULL argument");
   const supra_bf_config& c = h->cfg;
-  const int nx = c.out_dims[0], ny = c.out_dims[1], nz = c.out_dims[2], S = h->S, Lx = c.num_lines_x;
+  // entries encode base = (i0y Lx + i0x) Sd + k0 over the (decimated)
+  // line image (build_sc_tables)
+  const int nx = c.out_dims[0], ny = c.out_dims[1], nz = c.out_dims[2], S = h->Sd, Lx = c.num_lines_x;
   size_t n = 0;
   for (int iz = 0; iz < nz; iz++)
     for (int iy = 0; iy < ny; iy++)

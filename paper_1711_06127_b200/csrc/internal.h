@@ -87,12 +87,21 @@ struct DasArgs {
   int y_type;                  // SUPRA_T_F32 / SUPRA_T_U8
   unsigned* frame_max;         // [F] float bits (frame-max mode)
   int debug_skip;              // measurement only: skip the tap loop (TMA pipeline alone)
-  // [S/32] tensor maps in global memory identical to the launch's map except
-  // for the time extent: raw_maps[r - 1] has r rows in range, so a window box
-  // whose rows past the pass's last referenced row are out of bounds reads
-  // them as zeros without DRAM traffic (exact windows, one TMA per entry).
-  // NULL: every window uses the launch's map.
-  const CUtensorMap* raw_maps;
+  // 1: windows use the row-cut tensor maps of the launch's RawMaps kernel
+  // parameter (exact windows); 0: every window uses the launch's map
+  int row_cut;
+};
+
+// Row-cut tensor maps, passed BY VALUE as a __grid_constant__ kernel
+// parameter (16 KB; kernel parameters may be up to 32 KB since CUDA 12.1):
+// m[r - 1] is the launch's raw map with only r time rows in range, so a
+// window box whose rows past the pass's last referenced row are out of
+// bounds reads them as zeros without DRAM traffic (exact windows, one TMA
+// per entry).  Being a parameter, the set lives in the launch itself: no
+// device allocation, no host synchronisation, and a captured CUDA graph
+// keeps its own copy.
+struct RawMaps {
+  CUtensorMap m[kMaxSamples / kRowSamples];
 };
 
 struct EnvArgs {  // standalone epilogue on an RF buffer
@@ -193,7 +202,11 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // Launchers (return cudaGetLastError()).
 // raw is addressed through a 5-D tensor map {16 sample pairs (u32), S/32
 // rows, C, E, F} with box {16, das_rows_nt(nt), 1, 1, fb} for sh = das_shape().
-cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, DasShape sh, cudaStream_t st);
+// allow_warp: a single-frame CALL may use the warp-split kernel (its own sum
+// order); every multi-frame call, remainder launches included, uses
+// das_fused_kernel, whose results are bitwise independent of the batch.
+cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, const RawMaps& maps, DasShape sh,
+                       bool allow_warp, cudaStream_t st);
 DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps);
 // One frame per CTA (fb = 1) with the aperture split across warps
 // (das_warp.cu); same tensor map as launch_das for that shape.

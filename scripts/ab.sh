@@ -8,7 +8,7 @@ for v in $1; do
   for d in ${3:-0}; do
     for spec in $2; do
       c=${spec%%:*}; f=${spec##*:}
-      echo -n "$v dbg=$d "; SUPRA_BF_LIB=$lib SUPRA_BF_DEBUG=$d python scripts/quick_time.py $c $f 2>&1 | grep -E "beamform [0-9]"
+      echo -n "$v dbg=$d "; SUPRA_BF_DEBUG=$d python scripts/quick_time.py --lib=$lib $c $f 2>&1 | grep -E "beamform [0-9]"
     done
   done
 done

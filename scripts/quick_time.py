@@ -7,8 +7,13 @@ from paper_1711_06127_b200 import SupraBF
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 from gpu_util import raw_frames
 
-name = sys.argv[1] if len(sys.argv) > 1 else "C2"
-F = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+args = [a for a in sys.argv[1:] if not a.startswith("--lib=")]
+for a in sys.argv[1:]:
+    if a.startswith("--lib=") and a[6:]:
+        from paper_1711_06127_b200 import binding
+        binding.use_library(a[6:])
+name = args[0] if len(args) > 0 else "C2"
+F = int(args[1]) if len(args) > 1 else 100
 w = configs.CONFIGS[name]()
 w = w.replace(sc_output_type=configs.T_U8)
 t = time.time(); raw = raw_frames(w, F); torch.cuda.synchronize(); print("synth s", time.time() - t)

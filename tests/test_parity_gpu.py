@@ -132,7 +132,8 @@ def test_c2_batch_parity_and_batch_invariance():
         assert e_rf <= RF_TOL, (f, e_rf)
         assert e_db <= DB_TOL, (f, e_db)
     # frames are independent: any multi-frame batch gives bitwise the same
-    # result (one sum order per configuration) ...
+    # result (one sum order per configuration; all shapes are covered in
+    # test_parity_shapes_gpu.py) ...
     rf2, y2 = run_gpu(bf, raw[4:6], 2)
     assert np.array_equal(rf2[1], rf_g[5]) and np.array_equal(y2[1], y_g[5])
     # ... and a single frame (the warp-split kernel, its own sum order)
@@ -236,8 +237,9 @@ def test_c2_scan_conversion_indices():
 
 
 def test_c2_bench_launch_configuration():
-    """Full size, exactly the launch bench.py times: 100 frames per call (FB=8
-    frame groups incl. a ragged last group), f32 line image, u8 B-mode.
+    """Full size, exactly the launch bench.py times: 100 frames per call
+    (das_fused<16,4> over 96 frames + a <4,8> remainder launch for 4), f32
+    line image, u8 B-mode.
     Sampled frames vs the oracle chain: line image <= 0.01 dB, B-mode u8
     within 1 LSB of the oracle's u8 of its own scan conversion."""
     w = configs.c2(sc_output_type=configs.T_U8)
@@ -455,10 +457,10 @@ def test_c2_decimation_batch():
     assert np.max(np.abs(y_g[1].astype(int) - oracle.to_u8(y_o).astype(int))) <= 1
 
 
-# ------------------------- tensor-core FIR epilogue (16-frame batches, 65 taps)
+# ------------------------- FIR epilogue on 16-frame batches (<16,4>; 65 and 33 taps)
 @pytest.mark.parametrize("over", [dict(), dict(reference_mode=configs.REF_FIXED, reference_value=800.0,
                                                line_output_type=configs.T_U8),
-                                  dict(fir_taps=33)])            # 33 taps: the SIMT epilogue
+                                  dict(fir_taps=33)])            # 33 taps: shorter halos
 def test_c2_sixteen_frame_batch_epilogue(over):
     w = configs.c2(**over)
     F = 16
