@@ -191,9 +191,11 @@ __device__ __forceinline__ void band_env(const DasArgs& a, const float4* lineg, 
   }
 }
 
+// vout[q] = (line, frame) of the group's q-th (virtual) frame, frame < 0:
+// nothing to store (past the call's frames).
 template <int FB>
 __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int kbase, int o0, int o_end,
-                                          int line, int fg0, float* bmax) {
+                                          const int2* vout, float* bmax) {
   const int P = (a.fir_taps - 1) / 2;
   float env[4][4];
   band_env<0>(a, lineg, kbase, o0, P, env);
@@ -213,9 +215,10 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
     }
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      const int f = fg0 + q;
-      if (q >= FB || f >= a.F) break;
-      const size_t out = ((size_t)f * a.L + line) * a.Sd + kq;
+      if (q >= FB) break;
+      const int2 lf = vout[q];
+      if (lf.y < 0) continue;
+      const size_t out = ((size_t)lf.y * a.L + lf.x) * a.Sd + kq;
       const float e = env[o][q];
       if (a.ref_fixed) {
         const float y = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(e), a.log_k0), 0.f), 1.f) : 0.f;

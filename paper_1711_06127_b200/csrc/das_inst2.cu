@@ -2,8 +2,8 @@
 #include "das_kernel.cuh"
 
 namespace supra {
-template cudaError_t launch_k<8, 8, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
-template cudaError_t launch_k<4, 8, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
-template cudaError_t launch_k<2, 8, false>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
-template cudaError_t launch_k<1, 8, true>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+template cudaError_t launch_k<8, 8, false, 1>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+template cudaError_t launch_k<4, 8, true, 1>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+template cudaError_t launch_k<2, 8, false, 1>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+template cudaError_t launch_k<1, 8, true, 1>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 }  // namespace supra

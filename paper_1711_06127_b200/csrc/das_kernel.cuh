@@ -51,6 +51,8 @@ struct SmemLayout {
   uint64_t* full;   // [kMaxStages]
   unsigned* rel;    // [kMaxStages] warps done with the slot (last one refills it)
   unsigned* smax;   // [16] per-frame envelope max (float bits)
+  int2* vout;       // [16] (line, frame) of every virtual frame
+  int2* slot;       // [4] (event, mirror variant) of every line slot
 };
 
 // Bytes of everything except the ring; ring stages fill the rest of the
@@ -58,7 +60,7 @@ struct SmemLayout {
 __host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P) {
   return align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
          align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1)) + align128(sizeof(uint64_t) * kMaxStages) +
-         align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16);
+         align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16) + align128(sizeof(int2) * 20);
 }
 // CTAs per SM: 3 for short passes (NT = 2: 32 accumulators, <= 85
 // registers), else 2; the per-CTA shared-memory budget follows.
@@ -84,11 +86,12 @@ __host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int
   off[4] = o; o = align128(o + sizeof(uint64_t) * kMaxStages);
   off[5] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
   off[6] = o; o = align128(o + sizeof(unsigned) * 16);
+  off[7] = o; o = align128(o + sizeof(int2) * 20);
   return o;
 }
 
 __device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT, int nent_max, int P) {
-  size_t off[7];
+  size_t off[8];
   layout_bytes(FB, NT, nent_max, P, off);
   SmemLayout L;
   L.stage = (int16_t*)(base + off[0]);
@@ -99,6 +102,8 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT,
   L.full = (uint64_t*)(base + off[4]);
   L.rel = (unsigned*)(base + off[5]);
   L.smax = (unsigned*)(base + off[6]);
+  L.vout = (int2*)(base + off[7]);
+  L.slot = L.vout + 16;
   return L;
 }
 
@@ -268,29 +273,35 @@ __device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const fl
   }
 }
 
-template <int FB, int NT, bool T0>
+// FB frames x MIR mirror lines = VF virtual frames per CTA.  Virtual frame
+// v = m FB + f is frame f of the CTA's line slot m; the stage holds the
+// windows [v][rows][32] (one TMA per slot, FB frames each), and the tap
+// geometry computed for the primary line is applied to all VF.
+template <int FB, int NT, bool T0, int MIR>
 __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const DasArgs a,
                                                           const __grid_constant__ RawMaps rmaps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int VF = FB * MIR;
   constexpr int PL = NT * kTileK;                 // samples per pass
   constexpr int FR = (NT * 8 + 2) * kRowSamples;  // int16 elements per frame in a stage
   const int S = a.S;
   const int P = (a.fir_taps - 1) / 2;
-  const size_t SB = stage_bytes(FB, NT * 8 + 2);
-  SmemLayout sm = carve(smem_raw, FB, NT, a.entries_per_group, P);
-  const int line = a.line0 + blockIdx.x;
+  const size_t SB = stage_bytes(VF, NT * 8 + 2);
+  SmemLayout sm = carve(smem_raw, VF, NT, a.entries_per_group, P);
+  const int32_t* cd = a.cta + (size_t)(a.cta_base + (int)blockIdx.x) * 9;
+  const int pline = cd[0];          // primary line: group, direction, entry order
   const int fm = blockIdx.y * FB;   // first frame of the CTA in the tensor map
   const int f0 = a.fbase + fm;      // ... and in the call
   if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int g = a.line_group[line];
+  const int g = a.line_group[pline];
   const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
+  const int32_t* __restrict__ ech = a.ech + (size_t)g * a.entries_per_group * 4;
   const int nent = a.nentries[g];
   const int lane = threadIdx.x & 31;
-  const int ev = a.line_event[line];
-  const float4 dir = a.line_dir[line];
-  const int NS = das_stages(FB, NT, a.entries_per_group, P);
-  const int ng = fir_groups(FB);
+  const float4 dir = a.line_dir[pline];
+  const int NS = das_stages(VF, NT, a.entries_per_group, P);
+  const int ng = fir_groups(VF);
   const int span = fir_span(PL, P);
 
   if (threadIdx.x == 0) {
@@ -304,7 +315,13 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
   if (a.row_cut && (int)threadIdx.x < S / kRowSamples)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&rmaps.m[threadIdx.x]))
                  : "memory");
-  if (threadIdx.x < 16) sm.smax[threadIdx.x] = 0u;
+  if (threadIdx.x < 16) {
+    sm.smax[threadIdx.x] = 0u;
+    // output (line, frame) of virtual frame v; frame -1: none
+    const int v = threadIdx.x, m = v < VF ? v / FB : 0;
+    sm.vout[v] = make_int2(cd[1 + m], (v < VF && f0 + v % FB < a.F) ? f0 + v % FB : -1);
+    if (v < MIR) sm.slot[v] = make_int2(a.line_event[cd[1 + v]], cd[5 + v]);
+  }
 
   const int kt = threadIdx.x;
   const int kwarp_last = (kt | 31);
@@ -312,9 +329,10 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
   int curg = -1;
   int buf = 0;           // ring slot of the next entry (continues across passes)
   unsigned phase = 0;    // its mbarrier parity
-  auto flush_max = [&]() {
+  auto flush_max = [&]() {  // per real frame (v % FB)
     if (curg >= 0 && !a.ref_fixed)
-      for (int q = 0; q < 4 && 4 * curg + q < FB; q++) atomicMax(&sm.smax[4 * curg + q], __float_as_uint(bmax[q]));
+      for (int q = 0; q < 4 && 4 * curg + q < VF; q++)
+        atomicMax(&sm.smax[(4 * curg + q) % FB], __float_as_uint(bmax[q]));
   };
 
   for (int k0 = 0; k0 < S; k0 += PL) {
@@ -363,7 +381,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       const float tl = (float)kl + split_delay(Ah, B, hl, kl > 0 ? hl * hl : 1e-20f) + a.t0fs;
       const int rcut = max(1, min(S / kRowSamples, ((int)floorf(tl) + 3 + kRowSamples - 1) / kRowSamples));
       sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(e.kenter));
-      sm.wse[i] = make_int2(ws, e.elem | (rcut << 20));
+      sm.wse[i] = make_int2(ws, ei | (rcut << 20));
     }
     __syncthreads();  // records visible; the previous pass is done with the line buffer
 
@@ -373,9 +391,14 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       // rows at or past rcut are out of bounds in rmaps.m[rcut - 1]: zero
       // fill, no DRAM read (the box size, and so the tx count, is fixed)
       const CUtensorMap* m = a.row_cut ? &rmaps.m[(we.y >> 20) - 1] : &tmap;
-      mbar_arrive_tx(&sm.full[buf], (unsigned)(FB * FR * 2));
-      tma_load_5d((unsigned char*)sm.stage + buf * SB, m, 0, we.x / kRowSamples, we.y & 0xFFFFF, ev, fm,
-                  &sm.full[buf]);
+      const int ei = we.y & 0xFFFFF;
+      mbar_arrive_tx(&sm.full[buf], (unsigned)(VF * FR * 2));
+#pragma unroll
+      for (int s = 0; s < MIR; s++) {  // slot s: its event, its mirrored channel
+        const int2 sl = sm.slot[s];
+        tma_load_5d((unsigned char*)sm.stage + buf * SB + (size_t)s * FB * FR * 2, m, 0, we.x / kRowSamples,
+                    ech[ei * 4 + sl.y], sl.x, fm, &sm.full[buf]);
+      }
     };
     if (threadIdx.x == 0 && a.debug_skip != 2) {
       // the ring was last written through the generic proxy (line buffer)
@@ -383,7 +406,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       for (int jj = 0, b = buf; jj < NS && jj < np; jj++, b = (b + 1 == NS ? 0 : b + 1)) produce(jj, b);
     }
 
-    Acc<FB, NT> acc;
+    Acc<VF, NT> acc;
     acc.zero();
     const float kt0f = (float)(k0 + kt);
     for (int j = 0; j < np; j++) {
@@ -399,7 +422,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       int m0 = kenter - k0 - kwarp_last;
       m0 = m0 <= 0 ? 0 : (m0 + kTileK - 1) / kTileK;
       if (a.debug_skip != 1 && m0 < NT)
-        dispatch_tiles<FB, NT, T0>(m0 / tile_gran(NT), a, r, kenter, wsm, st, kt, k0, kt0f, acc);
+        dispatch_tiles<VF, NT, T0>(m0 / tile_gran(NT), a, r, kenter, wsm, st, kt, k0, kt0f, acc);
       // release the slot; the last warp to release it refills it (no warp
       // ever waits for another to issue a copy)
       __syncwarp();
@@ -426,37 +449,39 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       const int k = k0 + m * kTileK + kt;
-      float v[FB];
+      float v[VF];
       if (k < S) {
         const int n = (int)ncount[k];
         const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
-        if constexpr (FB == 1) {
+        if constexpr (VF == 1) {
           v[0] = acc.s(m) * inv;
         } else {
 #pragma unroll
-          for (int q = 0; q < FB / 2; q++) {
+          for (int q = 0; q < VF / 2; q++) {
             v[2 * q] = acc.p[m][q].x * inv;
             v[2 * q + 1] = acc.p[m][q].y * inv;
           }
         }
         if (a.rf) {
 #pragma unroll
-          for (int b = 0; b < FB; b++)
-            if (f0 + b < a.F) a.rf[((size_t)(f0 + b) * a.L + line) * S + k] = v[b];
+          for (int b = 0; b < VF; b++) {
+            const int2 lf = sm.vout[b];
+            if (lf.y >= 0) a.rf[((size_t)lf.y * a.L + lf.x) * S + k] = v[b];
+          }
         }
       } else {
 #pragma unroll
-        for (int b = 0; b < FB; b++) v[b] = 0.f;  // zero padding past the record
+        for (int b = 0; b < VF; b++) v[b] = 0.f;  // zero padding past the record
       }
       if (a.do_epilogue) {
         const int pk = fir_pad(k - kbase);
 #pragma unroll
-        for (int q4 = 0; q4 < (FB + 3) / 4; q4++) {
+        for (int q4 = 0; q4 < (VF + 3) / 4; q4++) {
           float4 x;
           x.x = v[4 * q4];
-          x.y = (4 * q4 + 1 < FB) ? v[(4 * q4 + 1) % FB] : 0.f;
-          x.z = (4 * q4 + 2 < FB) ? v[(4 * q4 + 2) % FB] : 0.f;
-          x.w = (4 * q4 + 3 < FB) ? v[(4 * q4 + 3) % FB] : 0.f;
+          x.y = (4 * q4 + 1 < VF) ? v[(4 * q4 + 1) % VF] : 0.f;
+          x.z = (4 * q4 + 2 < VF) ? v[(4 * q4 + 2) % VF] : 0.f;
+          x.w = (4 * q4 + 3 < VF) ? v[(4 * q4 + 3) % VF] : 0.f;
           sm.line[(size_t)q4 * span + pk] = x;
         }
       }
@@ -484,7 +509,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
         curg = q4;
         bmax[0] = bmax[1] = bmax[2] = bmax[3] = 0.f;
       }
-      fir_block<FB>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, line, f0 + 4 * q4, bmax);
+      fir_block<VF>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, sm.vout + 4 * q4, bmax);
     }
     // RF tail k in [k0 + PL - 2P, k0 + PL) for the next pass's first outputs
     if (kend < S)
@@ -507,18 +532,18 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
 }
 
 inline size_t das_smem_bytes_impl(int FB, int NT, int nent_max, int fir_taps) {
-  size_t off[7];
+  size_t off[8];
   return layout_bytes(FB, NT, nent_max, (fir_taps - 1) / 2, off);
 }
 
-template <int FB, int NT, bool T0>
+template <int FB, int NT, bool T0, int MIR>
 cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, const RawMaps& maps, cudaStream_t st) {
-  const size_t smem = das_smem_bytes_impl(FB, NT, a.entries_per_group, a.fir_taps);
-  auto kern = das_fused_kernel<FB, NT, T0>;
+  const size_t smem = das_smem_bytes_impl(FB * MIR, NT, a.entries_per_group, a.fir_taps);
+  auto kern = das_fused_kernel<FB, NT, T0, MIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.nlines, (a.Fmap + FB - 1) / FB);
+  cfg.gridDim = dim3(a.nlines / MIR, (a.Fmap + FB - 1) / FB);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

@@ -209,12 +209,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
   const int fm = blockIdx.y;
   const int f0 = a.fbase + fm;
   if (a.pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int g = a.line_group[line];
+  // (primary line, mirror variant) of this line (DasArgs::cta, MIR = 1):
+  // the primary's group, direction and entry order, the variant's channels
+  const int pline = a.cta[(size_t)line * 9], var = a.cta[(size_t)line * 9 + 5];
+  const int g = a.line_group[pline];
   const DasEntry* __restrict__ ents = a.entries + (size_t)g * a.entries_per_group;
+  const int32_t* __restrict__ ech = a.ech + (size_t)g * a.entries_per_group * 4;
   const int np = a.nentries[g];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ev = a.line_event[line];
-  const float4 dir = a.line_dir[line];
+  const float4 dir = a.line_dir[pline];
 
   // 1/max(k,1) for tile pairs: rkt[p*32 + l] = (k = 64p + l, k + 32)
   for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     const int ws = entry_ws(e, dir, a.t0fs, Ah, B);
     uint64_t* bar = &full[warp * kMaxWarpStages + slot];
     mbar_arrive_tx(bar, (unsigned)(ROWS * kRowSamples * 2));
-    tma_load_5d(ring + (size_t)(warp * NSW + slot) * SB, &tmap, 0, ws / kRowSamples, e.elem, ev, fm, bar);
+    tma_load_5d(ring + (size_t)(warp * NSW + slot) * SB, &tmap, 0, ws / kRowSamples, ech[j * 4 + var], ev, fm, bar);
   };
   if (lane == 0 && a.debug_skip != 2)
     for (int s = 0; s < NSW; s++)
@@ -311,8 +315,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     lineb[fir_pad(i < 2 * P ? i : S + i)] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
   float bmax[4] = {0.f, 0.f, 0.f, 0.f};
+  const int2 vout[1] = {make_int2(line, f0)};
   for (int it = threadIdx.x; it < S / 4; it += blockDim.x)
-    fir_block<1>(a, lineb, kbase, 4 * it, S, line, f0, bmax);
+    fir_block<1>(a, lineb, kbase, 4 * it, S, vout, bmax);
   if (!a.ref_fixed) {
     atomicMax(&smax[0], __float_as_uint(bmax[0]));
     __syncthreads();

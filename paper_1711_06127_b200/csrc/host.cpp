@@ -68,6 +68,14 @@ struct supra_bf {
   uint16_t* d_ncount = nullptr;
   float4* d_line_dir = nullptr;
   int32_t* d_line_event = nullptr;
+  // mirror symmetry (DasArgs::cta / ech): CTA descriptor tables for MIR = 1,
+  // 2, 4 lines per CTA (index 0, 1, 2; NULL if the layout lacks that order)
+  // and the per-entry channel of each mirror variant
+  int32_t* d_cta[3] = {nullptr, nullptr, nullptr};
+  int32_t* d_ech = nullptr;
+  int sym_order = 1;    // 1, 2 or 4 mirror lines that share one delay set
+  bool sym_x = false;   // the 2-line tables pair x-mirrors (rows stay whole)
+  int num_sms = 148;
   float2* d_fir = nullptr;
   unsigned* d_frame_max = nullptr;
   float* d_env = nullptr;
@@ -118,7 +126,8 @@ cudaError_t upload(T** d, const std::vector<T>& h) {
 }
 
 void free_all(supra_bf* h) {
-  void* ptrs[] = {h->d_line_group, h->d_entries, h->d_nentries, h->d_ncount, h->d_line_dir, h->d_line_event,
+  void* ptrs[] = {h->d_cta[0], h->d_cta[1], h->d_cta[2], h->d_ech,
+                  h->d_line_group, h->d_entries, h->d_nentries, h->d_ncount, h->d_line_dir, h->d_line_event,
                   h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_blk_kmin, h->d_col_l0, h->d_col_nl, h->d_rows, h->d_ent};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -279,6 +288,119 @@ supra_status validate(const supra_bf_config* c) {
   return SUPRA_OK;
 }
 
+// ---- mirror symmetry -------------------------------------------------
+// A phased / matrix layout (every origin at 0) whose steering grid is
+// symmetric about the x (y) axis pairs line (lx, ly) with (Lx-1-lx, ly)
+// ((lx, Ly-1-ly)).  With element (i, j) <-> (Nx-1-i, j) ((i, Ny-1-j)) the
+// mirrored line sees the mirrored element at exactly the same q-component
+// products d.q, |q|^2 and rho (sign flips cancel in IEEE arithmetic), so
+// its delays, weights, memberships and N(k) are bitwise those of the
+// original: up to 4 lines share one delay set, and the DAS kernel computes
+// the geometry once for all of them ("mirror lines").
+// Every line is described as (canonical primary line, variant v): variant
+// bit 0 = x-mirror, bit 1 = y-mirror; its taps are the primary's aperture
+// entries in the primary's order, each read from the variant's mirrored
+// channel -- so a line's result does not depend on how lines are grouped
+// into CTAs.  Returns the CTA tables and entry channels, or sym_order = 1.
+void build_mirror_tables(supra_bf* h, const std::vector<int32_t>& line_group,
+                         const std::vector<std::vector<DasEntry>>& groups, const std::vector<int>& g_event,
+                         std::vector<int32_t>& cta1, std::vector<int32_t>& cta2, std::vector<int32_t>& cta4,
+                         std::vector<int32_t>& ech, int per) {
+  const supra_bf_config& c = h->cfg;
+  const int L = h->L, Lx = c.num_lines_x, Ly = c.num_lines_y, Nx = c.elements_x, Ny = c.elements_y;
+  const int G = (int)groups.size();
+  // channel of an element: identity, or the (uniform) channel map
+  const int nel = Nx * Ny;
+  std::vector<int> chan_of(nel, -1);
+  bool ok = true;
+  if (c.num_channels > 0) {
+    for (int e = 1; e < c.num_events && ok; e++)
+      ok = std::equal(c.channel_element, c.channel_element + c.num_channels,
+                      c.channel_element + (size_t)e * c.num_channels);
+    for (int ch = 0; ch < c.num_channels && ok; ch++)
+      if (c.channel_element[ch] >= 0) chan_of[c.channel_element[ch]] = ch;
+  } else {
+    for (int e = 0; e < nel; e++) chan_of[e] = e;
+  }
+  for (int l = 0; l < L && ok; l++)
+    ok = c.line_origin_mm[3 * l] == 0.0 && c.line_origin_mm[3 * l + 1] == 0.0 && c.line_origin_mm[3 * l + 2] == 0.0;
+  auto mirror_el = [&](int e, int v) {
+    int i = e % Nx, j = e / Nx;
+    if (v & 1) i = Nx - 1 - i;
+    if (v & 2) j = Ny - 1 - j;
+    return j * Nx + i;
+  };
+  auto mirror_line = [&](int l, int v) {
+    int lx = l % Lx, ly = l / Lx;
+    if (v & 1) lx = Lx - 1 - lx;
+    if (v & 2) ly = Ly - 1 - ly;
+    return ly * Lx + lx;
+  };
+  auto fdir = [&](int l, int k) { return (float)c.line_direction[3 * l + k]; };
+  auto sym_ok = [&](int v) {
+    if (!ok) return false;
+    if ((v & 1) && Lx % 2) return false;
+    if ((v & 2) && (Ly % 2 || Ly < 2)) return false;
+    for (int l = 0; l < L; l++) {
+      const int m = mirror_line(l, v);
+      const float ex = (v & 1) ? -fdir(l, 0) : fdir(l, 0), ey = (v & 2) ? -fdir(l, 1) : fdir(l, 1);
+      if (fdir(m, 0) != ex || fdir(m, 1) != ey || fdir(m, 2) != fdir(l, 2)) return false;
+      if (line_group[m] != line_group[l]) return false;
+    }
+    // the recorded element set is closed under the mirror
+    for (int e = 0; e < nel; e++)
+      if ((chan_of[e] >= 0) != (chan_of[mirror_el(e, v)] >= 0)) return false;
+    return true;
+  };
+  const bool sx = sym_ok(1), sy = sym_ok(2);
+  const int vmask = (sx ? 1 : 0) | (sy ? 2 : 0);
+  h->sym_order = (sx ? 2 : 1) * (sy ? 2 : 1);
+  h->sym_x = sx;
+  // canonical primary and variant of every line
+  std::vector<int> prim(L), var(L);
+  for (int l = 0; l < L; l++) {
+    const int lx = l % Lx, ly = l / Lx;
+    int v = 0;
+    if ((vmask & 1) && lx >= Lx / 2) v |= 1;
+    if ((vmask & 2) && ly >= Ly / 2) v |= 2;
+    var[l] = v;
+    prim[l] = mirror_line(l, v);
+  }
+  // entry channels per variant (variant 0 = the entry's own channel)
+  ech.assign((size_t)G * per * 4, 0);
+  for (int g = 0; g < G; g++)
+    for (size_t j = 0; j < groups[g].size(); j++) {
+      const int ch = groups[g][j].elem;
+      const int el = c.num_channels > 0 ? c.channel_element[(size_t)g_event[g] * c.num_channels + ch] : ch;
+      for (int v = 0; v < 4; v++) {
+        const int mc = (v & ~vmask) ? ch : chan_of[mirror_el(el, v)];
+        ech[((size_t)g * per + j) * 4 + v] = mc < 0 ? ch : mc;
+      }
+    }
+  auto push = [](std::vector<int32_t>& t, int p, const int* ls, const int* vs, int n) {
+    t.push_back(p);
+    for (int i = 0; i < 4; i++) t.push_back(i < n ? ls[i] : ls[0]);
+    for (int i = 0; i < 4; i++) t.push_back(i < n ? vs[i] : vs[0]);
+  };
+  cta1.clear(); cta2.clear(); cta4.clear();
+  for (int l = 0; l < L; l++) push(cta1, prim[l], &l, &var[l], 1);
+  if (h->sym_order >= 2) {
+    // pairs along one mirrored axis (x if available): slots {l, mirror(l)}
+    const int vb = (vmask & 1) ? 1 : 2;
+    for (int l = 0; l < L; l++) {
+      if (var[l] & vb) continue;  // l is the first slot of its pair
+      const int ls[2] = {l, mirror_line(l, vb)}, vs[2] = {var[l], var[l] | vb};
+      push(cta2, prim[l], ls, vs, 2);
+    }
+  }
+  if (h->sym_order == 4)
+    for (int l = 0; l < L; l++) {
+      if (var[l]) continue;
+      const int ls[4] = {l, mirror_line(l, 1), mirror_line(l, 2), mirror_line(l, 3)}, vs[4] = {0, 1, 2, 3};
+      push(cta4, l, ls, vs, 4);
+    }
+}
+
 // ---- DAS tables ------------------------------------------------------
 supra_status build_das_tables(supra_bf* h) {
   const supra_bf_config& c = h->cfg;
@@ -397,7 +519,13 @@ supra_status build_das_tables(supra_bf* h) {
       h->fir_s[(size_t)b * (kMaxHalfTaps + 1) + j] = fir[(size_t)b * T + j + P].y;
     }
   }
+  std::vector<int32_t> cta1, cta2, cta4, ech;
+  build_mirror_tables(h, line_group, groups, g_event, cta1, cta2, cta4, ech, per);
   cudaError_t e;
+  if ((e = upload(&h->d_cta[0], cta1)) != cudaSuccess || (e = upload(&h->d_cta[1], cta2)) != cudaSuccess ||
+      (e = upload(&h->d_cta[2], cta4)) != cudaSuccess || (e = upload(&h->d_ech, ech)) != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "table upload: %s",
+                cudaGetErrorString(e));
   if ((e = upload(&h->d_line_group, line_group)) != cudaSuccess ||
       (e = upload(&h->d_entries, flat)) != cudaSuccess || (e = upload(&h->d_nentries, nentries)) != cudaSuccess ||
       (e = upload(&h->d_ncount, ncount)) != cudaSuccess ||
@@ -688,6 +816,36 @@ void fill_log(const supra_bf* h, int& fixed, float& k1, float& k0) {
 
 }  // namespace
 
+// DAS launch shape for `frames` frames: mirror lines per CTA (up to
+// mir_max) as many as the layout's symmetry order gives while the grid keeps
+// >= 2 CTAs per SM, else one line per CTA.
+static DasShape pick_shape(supra_bf* h, int frames, int mir_max) {
+  const supra_bf_config& c = h->cfg;
+  int force = 0;
+#ifdef SUPRA_DEV_KNOBS
+  if (const char* ev = std::getenv("SUPRA_BF_MIR")) force = std::atoi(ev);  // A/B measurements only
+#endif
+  for (int m = 4; m >= 2; m /= 2) {
+    if (m > mir_max || (force && force != m)) continue;
+    const DasShape sh = das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps, m);
+    if (sh.fb == 0) continue;
+    const long ncta = (long)(h->L / m) * ((frames + sh.fb / m - 1) / (sh.fb / m));
+    if (force || ncta >= 2L * h->num_sms) return sh;
+  }
+  return das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps, 1);
+}
+
+// Largest mirror order usable for lines [line0, line0 + nlines): the whole
+// volume takes the layout's order; whole rows of lines take x-mirror pairs.
+// t0 != 0 (or nearest-sample lookup) uses one line per CTA.
+static int mirror_max(const supra_bf* h, int line0, int nlines, float t0fs) {
+  if (t0fs != 0.f || h->sym_order == 1) return 1;
+  if (line0 == 0 && nlines == h->L) return h->sym_order;
+  const int Lx = h->cfg.num_lines_x;
+  if (h->sym_x && line0 % Lx == 0 && nlines % Lx == 0) return 2;
+  return 1;
+}
+
 extern "C" {
 
 const char* supra_bf_last_error(void) { return g_err.c_str(); }
@@ -738,7 +896,14 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   }
 #endif
   h->mcache.reserve(supra_bf::kMapCache);  // entries never move (launches point into them)
-  const DasShape sh = das_shape(h->frames_per_cta, h->S, maxF, h->entries_per_group, cfg->fir_taps);
+  {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg->device) == cudaSuccess && nsm > 0)
+      h->num_sms = nsm;
+  }
+  const bool t0zero = (float)(cfg->t0_s * cfg->sample_frequency_hz +
+                              (cfg->interpolation == SUPRA_INTERP_NEAREST ? 0.5 : 0.0)) == 0.f;
+  const DasShape sh = pick_shape(h, maxF, t0zero ? h->sym_order : 1);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
   // f32 line-domain scratch [maxF][L][S/dec]: the envelope of a frame-max
   // call with a u8 line image, and supra_bf_beamform_bmode's envelope / y
@@ -749,8 +914,8 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
     return fail(SUPRA_E_RESOURCE, "scratch allocation: %s", cudaGetErrorString(e));
   }
   // kernels per beamform call at max_frames_per_call: DAS (+ remainder DAS) (+ finalize)
-  h->info[0] = 1 + (maxF % sh.fb != 0) + (cfg->reference_mode == SUPRA_REF_FRAME_MAX);
-  h->info[1] = sh.fb;
+  h->info[0] = 1 + (maxF % (sh.fb / sh.mir) != 0) + (cfg->reference_mode == SUPRA_REF_FRAME_MAX);
+  h->info[1] = sh.fb / sh.mir;
   h->info[2] = (int64_t)sh.nt * kTileK;
   *out = h;
   return SUPRA_OK;
@@ -797,6 +962,7 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   a.dec = h->dec;
   a.L = h->L;
   a.entries_per_group = h->entries_per_group;
+  a.ech = h->d_ech;
   a.line_group = h->d_line_group;
   a.entries = h->d_entries;
   a.nentries = h->d_nentries;
@@ -853,18 +1019,26 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
-  // Frames in groups of sh.fb per CTA; a remainder (frames % fb) runs as a
+  // Mirror lines per CTA (build_mirror_tables): the largest order the
+  // layout has whose grid still fills the GPU (>= 2 CTAs per SM); results
+  // do not depend on the choice.  Whole-volume calls with t0 = 0 only.
+  const int mmax = mirror_max(h, line0, nlines, a.t0fs);
+  const DasShape sh = pick_shape(h, frames, mmax);
+  const int fbr = sh.fb / sh.mir;  // frames per CTA
+  a.cta = h->d_cta[sh.mir == 4 ? 2 : (sh.mir == 2 ? 1 : 0)];
+  a.cta_base = line0 / sh.mir;
+  // Frames in groups of fbr per CTA; a remainder (frames % fbr) runs as a
   // second, programmatically-serialised launch with its own (smaller) shape
   // that fills the SMs the first grid's tail leaves idle.
-  const DasShape sh = das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps);
-  const int Fmain = (frames / sh.fb) * sh.fb;
+  const int Fmain = (frames / fbr) * fbr;
   const int rem = frames - Fmain;
-  const DasShape sh2 = rem ? das_shape(h->frames_per_cta, h->S, rem, h->entries_per_group, c.fir_taps) : sh;
+  const DasShape sh2 = rem ? pick_shape(h, rem, mmax) : sh;
+  const int fbr2 = sh2.fb / sh2.mir;
   const size_t frame_bytes = (size_t)h->E * h->C * h->S * sizeof(int16_t);
   CUtensorMap tm, tm2;
-  if (!make_raw_map(&tm, raw, Fmain, h->E, h->C, h->S, das_rows_nt(sh.nt), sh.fb) ||
+  if (!make_raw_map(&tm, raw, Fmain, h->E, h->C, h->S, das_rows_nt(sh.nt), fbr) ||
       (rem && !make_raw_map(&tm2, (const char*)raw + Fmain * frame_bytes, rem, h->E, h->C, h->S,
-                            das_rows_nt(sh2.nt), sh2.fb)))
+                            das_rows_nt(sh2.nt), fbr2)))
     return fail(SUPRA_E_CUDA, "cuTensorMapEncodeTiled failed for the raw buffer");
   a.fbase = 0;
   a.Fmap = Fmain;
@@ -878,21 +1052,26 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
 #endif
   // the warp-split kernel only for a single-frame call; remainders of a
   // multi-frame call use das_fused_kernel (batch-independent results)
-  const bool warp1 = frames == 1 && das_warp_ok(sh.fb, h->S, a.t0fs);
+  // (not for mirror-symmetric layouts: there every launch, whatever its
+  // lines per CTA, gives bitwise the same result)
+  const bool warp_ok = frames == 1 && h->sym_order == 1;
+  const bool warp1 = warp_ok && das_warp_ok(sh.fb, h->S, a.t0fs);
   static const RawMaps kNoMaps{};
-  const RawMaps* m1 = (exact && !warp1) ? row_cut_maps(h, raw, Fmain, sh.fb, sh.nt) : nullptr;
+  const RawMaps* m1 = (exact && !warp1) ? row_cut_maps(h, raw, Fmain, fbr, sh.nt) : nullptr;
   a.row_cut = m1 != nullptr;
   if (h->ev_before) cudaEventRecord(h->ev_before, st);
-  supra_status s = check_launch(launch_das(tm, a, m1 ? *m1 : kNoMaps, sh, frames == 1, st), "das kernel");
+  supra_status s = check_launch(launch_das(tm, a, m1 ? *m1 : kNoMaps, sh, warp_ok, st), "das kernel");
   if (s == SUPRA_OK && rem) {
     DasArgs a2 = a;
     a2.fbase = Fmain;
     a2.Fmap = rem;
     a2.pdl_trigger = 0;
     a2.pdl_wait_end = 1;
-    const RawMaps* m2 = exact ? row_cut_maps(h, (const char*)raw + Fmain * frame_bytes, rem, sh2.fb, sh2.nt)
+    const RawMaps* m2 = exact ? row_cut_maps(h, (const char*)raw + Fmain * frame_bytes, rem, fbr2, sh2.nt)
                               : nullptr;
     a2.row_cut = m2 != nullptr;
+    a2.cta = h->d_cta[sh2.mir == 4 ? 2 : (sh2.mir == 2 ? 1 : 0)];
+    a2.cta_base = line0 / sh2.mir;
     s = check_launch(launch_das(tm2, a2, m2 ? *m2 : kNoMaps, sh2, false, st), "das kernel (remainder frames)");
   }
   if (h->ev_after) cudaEventRecord(h->ev_after, st);

@@ -31,9 +31,10 @@ inline __host__ __device__ int das_nt(int S) {  // largest useful NT for S
   return t <= 4 ? 4 : (t <= 8 ? 8 : 16);
 }
 inline __host__ __device__ int das_rows_nt(int nt) { return nt * (kTileK / kRowSamples) + 2; }
-// DAS launch shape: frames per CTA (fb) x tiles per pass (nt), fb * nt <= 64.
+// DAS launch shape: virtual frames per CTA (fb = frames x mir mirror lines)
+// x tiles per pass (nt), fb * nt <= 64; mir lines share one delay set.
 struct DasShape {
-  int fb, nt;
+  int fb, nt, mir = 1;
 };
 
 // One receive-aperture entry of a line group (lines sharing an origin),
@@ -57,6 +58,15 @@ struct DasArgs {
   int fbase, Fmap;             // frames [fbase, fbase + Fmap) of the call, = frames [0, Fmap) of the tensor map
   int pdl_trigger;             // primary of a split call: let the secondary start on free SMs
   int pdl_wait_end;            // secondary: launched programmatically, retire after the primary
+  // CTA descriptors {primary line, line[4], variant[4]} for the launch's
+  // lines per CTA (MIR = 1: one per line; 2: x-mirror pairs, row-major over
+  // lx < Lx/2; 4: quads over lx < Lx/2, ly < Ly/2): the
+  // primary's group, direction and entry order serve every line of the
+  // CTA; slot s reads entry j from channel ech[g][j][variant[s]] (mirror
+  // symmetry, host.cpp build_mirror_tables)
+  const int32_t* cta;
+  int cta_base;                // descriptor of CTA b: cta[cta_base + b]
+  const int32_t* ech;          // [G][entries_per_group][4]
   const int32_t* line_group;   // [L]
   const DasEntry* entries;     // [G][entries_per_group], sorted by kenter (ascending)
   const int32_t* nentries;     // [G]: entries with kenter < S
@@ -207,7 +217,7 @@ __device__ __forceinline__ float lg2_approx(float x) {
 // das_fused_kernel, whose results are bitwise independent of the batch.
 cudaError_t launch_das(const CUtensorMap& raw_map, const DasArgs& a, const RawMaps& maps, DasShape sh,
                        bool allow_warp, cudaStream_t st);
-DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps);
+DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps, int mir = 1);
 // One frame per CTA (fb = 1) with the aperture split across warps
 // (das_warp.cu); same tensor map as launch_das for that shape.
 bool das_warp_ok(int fb, int S, float t0fs);

@@ -180,7 +180,9 @@ def test_batch_invariance_bitwise_c2():
     a = rf1[0].cpu().numpy().astype(np.float64)
     b = rf100[98].cpu().numpy().astype(np.float64)
     assert rf_err(a, b) <= 1e-6
-    assert db_err(li1[0].cpu().numpy(), li100[98].cpu().numpy().astype(np.float64)) <= 1e-4
+    # (RF within 1e-6 of the frame max moves a pixel at the -50 dB floor by
+    # up to 8.7 x 1e-6 / 10^(-50/20) = 2.8e-3 dB)
+    assert db_err(li1[0].cpu().numpy(), li100[98].cpu().numpy().astype(np.float64)) <= 5e-3
     # one frame against the oracle, from the 100-frame call
     rf_o, env_o = oracle_chain(w, raw[97].cpu().numpy())
     assert rf_err(rf100[97].cpu().numpy(), rf_o) <= RF_TOL
