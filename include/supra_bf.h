@@ -76,7 +76,8 @@ enum { SUPRA_SC_LINEAR_2D = 0, SUPRA_SC_SECTOR_2D = 1, SUPRA_SC_PYRAMID_3D = 2 }
 /*
  * Configuration.  `supra_bf_create` copies every field and array; the caller
  * may free them afterwards.  Ranges checked at create (else SUPRA_E_PARAM):
- *   elements_x, elements_y >= 1, pitch > 0, center_frequency > 0;
+ *   elements_x, elements_y >= 1 with elements_x * elements_y <= 65535 (and num_channels <= 65535),
+ *   pitch > 0, center_frequency > 0;
  *   num_events >= 1; samples_per_channel a multiple of 32 in [32, 4096]
  *   (one TMA box holds a whole trace in 64-byte rows; 4096 = 16 tiles of 256
  *   samples held in registers per thread); input_type = SUPRA_T_I16;

@@ -43,8 +43,8 @@ extern template cudaError_t launch_k<2, 4, false, 4>(const CUtensorMap&, const D
 extern template cudaError_t launch_k<2, 8, false, 4>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 extern template cudaError_t launch_k<4, 4, false, 4>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 
-size_t das_smem_bytes(int FB, int NT, int nent_max, int fir_taps) {
-  return das_smem_bytes_impl(FB, NT, nent_max, fir_taps);
+size_t das_smem_bytes(int FB, int NT, int nent_max, int fir_taps, int mir) {
+  return das_smem_bytes_impl(FB, NT, nent_max, fir_taps, mir);
 }
 
 // (virtual frames per CTA, tiles per pass) for `mir` mirror lines per CTA:
@@ -71,7 +71,7 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps, int mir
     if (ci < 0 && (mir != 1 || !((vf == 16 && nt == 4) || (vf == 8 && (nt == 4 || nt == 8))))) continue;
     const int fb = vf / mir;
     if (fb > fb_max || (fb > F && fb > 1) || nt > ntmax) continue;
-    const size_t fixed = fixed_bytes(vf, nent_max, P);
+    const size_t fixed = fixed_bytes(vf, nent_max, P, mir);
     const size_t ring = 3 * stage_bytes(vf, das_rows_nt(nt));
     const size_t fir = align128((size_t)fir_groups(vf) * fir_span(nt * kTileK, P) * 16);
     if (fixed + (ring > fir ? ring : fir) > das_smem_budget(nt)) continue;

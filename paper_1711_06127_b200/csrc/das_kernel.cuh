@@ -42,11 +42,14 @@ namespace supra {
 namespace {
 
 
+__device__ __forceinline__ int sel4(int4 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
+
 struct SmemLayout {
   int16_t* stage;   // [NS][stage_bytes]
   float4* line;     // FIR line buffer, aliases the stage ring between passes
   float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
-  int2* wse;        // [nent] {window start ws, channel | rcut << 20}
+  int2* wse;        // [nent] {window start ws, slot-0 channel | rcut << 20}
+  uint2* chx;       // [nent] (MIR > 1) channels of slots 0..3, 16 bits each
   float4* carry;    // [ngroups][2P] RF tail of the previous pass
   uint64_t* full;   // [kMaxStages]
   unsigned* rel;    // [kMaxStages] warps done with the slot (last one refills it)
@@ -57,8 +60,9 @@ struct SmemLayout {
 
 // Bytes of everything except the ring; ring stages fill the rest of the
 // per-CTA budget (2 CTAs per SM), between 3 and kMaxStages.
-__host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P) {
+__host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P, int MIR) {
   return align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
+         (MIR > 1 ? align128(sizeof(uint2) * nent_max) : 0) +
          align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1)) + align128(sizeof(uint64_t) * kMaxStages) +
          align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16) + align128(sizeof(int2) * 20);
 }
@@ -67,16 +71,16 @@ __host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P) {
 __host__ __device__ constexpr int das_ctas_per_sm(int NT) { return NT == 2 ? 3 : 2; }
 __host__ __device__ constexpr size_t das_smem_budget(int NT) { return NT == 2 ? 75 * 1024 : 113 * 1024; }
 
-__host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P) {
-  const size_t fixed = fixed_bytes(FB, nent_max, P);
+__host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P, int MIR) {
+  const size_t fixed = fixed_bytes(FB, nent_max, P, MIR);
   const size_t sb = stage_bytes(FB, das_rows_nt(NT));
   const size_t budget = das_smem_budget(NT);
   const long n = fixed >= budget ? 0 : (long)((budget - fixed) / sb);
   return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : (int)n);
 }
 
-__host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int P, size_t* off) {
-  const size_t ring = (size_t)das_stages(FB, NT, nent_max, P) * stage_bytes(FB, das_rows_nt(NT));
+__host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int P, int MIR, size_t* off) {
+  const size_t ring = (size_t)das_stages(FB, NT, nent_max, P, MIR) * stage_bytes(FB, das_rows_nt(NT));
   const size_t fb = align128((size_t)fir_groups(FB) * fir_span(NT * kTileK, P) * 16);
   size_t o = 0;
   off[0] = o; o = align128(o + (ring > fb ? ring : fb));
@@ -87,12 +91,13 @@ __host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int
   off[5] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
   off[6] = o; o = align128(o + sizeof(unsigned) * 16);
   off[7] = o; o = align128(o + sizeof(int2) * 20);
+  off[8] = o; o = MIR > 1 ? align128(o + sizeof(uint2) * nent_max) : o;
   return o;
 }
 
-__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT, int nent_max, int P) {
-  size_t off[8];
-  layout_bytes(FB, NT, nent_max, P, off);
+__device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT, int nent_max, int P, int MIR) {
+  size_t off[9];
+  layout_bytes(FB, NT, nent_max, P, MIR, off);
   SmemLayout L;
   L.stage = (int16_t*)(base + off[0]);
   L.line = (float4*)(base + off[0]);
@@ -104,6 +109,7 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT,
   L.smax = (unsigned*)(base + off[6]);
   L.vout = (int2*)(base + off[7]);
   L.slot = L.vout + 16;
+  L.chx = (uint2*)(base + off[8]);
   return L;
 }
 
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
   const int S = a.S;
   const int P = (a.fir_taps - 1) / 2;
   const size_t SB = stage_bytes(VF, NT * 8 + 2);
-  SmemLayout sm = carve(smem_raw, VF, NT, a.entries_per_group, P);
+  SmemLayout sm = carve(smem_raw, VF, NT, a.entries_per_group, P, MIR);
   const int32_t* cd = a.cta + (size_t)(a.cta_base + (int)blockIdx.x) * 9;
   const int pline = cd[0];          // primary line: group, direction, entry order
   const int fm = blockIdx.y * FB;   // first frame of the CTA in the tensor map
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
   const int nent = a.nentries[g];
   const int lane = threadIdx.x & 31;
   const float4 dir = a.line_dir[pline];
-  const int NS = das_stages(VF, NT, a.entries_per_group, P);
+  const int NS = das_stages(VF, NT, a.entries_per_group, P, MIR);
   const int ng = fir_groups(VF);
   const int span = fir_span(PL, P);
 
@@ -381,7 +387,15 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       const float tl = (float)kl + split_delay(Ah, B, hl, kl > 0 ? hl * hl : 1e-20f) + a.t0fs;
       const int rcut = max(1, min(S / kRowSamples, ((int)floorf(tl) + 3 + kRowSamples - 1) / kRowSamples));
       sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(e.kenter));
-      sm.wse[i] = make_int2(ws, ei | (rcut << 20));
+      // channels of the line slots, resolved here (off the refill path:
+      // a global load in produce() would sit between a slot's release and
+      // its refill)
+      const int4 ch4 = *reinterpret_cast<const int4*>(ech + (size_t)ei * 4);
+      const int c0 = sel4(ch4, sm.slot[0].y);
+      sm.wse[i] = make_int2(ws, c0 | (rcut << 20));
+      if constexpr (MIR > 1)
+        sm.chx[i] = make_uint2((unsigned)c0 | ((unsigned)sel4(ch4, sm.slot[1].y) << 16),
+                               MIR > 2 ? (unsigned)sel4(ch4, sm.slot[2].y) | ((unsigned)sel4(ch4, sm.slot[3].y) << 16) : 0u);
     }
     __syncthreads();  // records visible; the previous pass is done with the line buffer
 
@@ -391,13 +405,18 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
       // rows at or past rcut are out of bounds in rmaps.m[rcut - 1]: zero
       // fill, no DRAM read (the box size, and so the tx count, is fixed)
       const CUtensorMap* m = a.row_cut ? &rmaps.m[(we.y >> 20) - 1] : &tmap;
-      const int ei = we.y & 0xFFFFF;
       mbar_arrive_tx(&sm.full[buf], (unsigned)(VF * FR * 2));
+      if constexpr (MIR == 1) {
+        tma_load_5d((unsigned char*)sm.stage + buf * SB, m, 0, we.x / kRowSamples, we.y & 0xFFFFF, sm.slot[0].x, fm,
+                    &sm.full[buf]);
+      } else {
+        const uint2 cx = sm.chx[jj];
 #pragma unroll
-      for (int s = 0; s < MIR; s++) {  // slot s: its event, its mirrored channel
-        const int2 sl = sm.slot[s];
-        tma_load_5d((unsigned char*)sm.stage + buf * SB + (size_t)s * FB * FR * 2, m, 0, we.x / kRowSamples,
-                    ech[ei * 4 + sl.y], sl.x, fm, &sm.full[buf]);
+        for (int s = 0; s < MIR; s++) {  // slot s: its event, its mirrored channel
+          const unsigned w = s < 2 ? cx.x : cx.y;
+          tma_load_5d((unsigned char*)sm.stage + buf * SB + (size_t)s * FB * FR * 2, m, 0, we.x / kRowSamples,
+                      (int)((s & 1) ? w >> 16 : w & 0xFFFFu), sm.slot[s].x, fm, &sm.full[buf]);
+        }
       }
     };
     if (threadIdx.x == 0 && a.debug_skip != 2) {
@@ -531,14 +550,14 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
   if (a.pdl_wait_end) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-inline size_t das_smem_bytes_impl(int FB, int NT, int nent_max, int fir_taps) {
-  size_t off[8];
-  return layout_bytes(FB, NT, nent_max, (fir_taps - 1) / 2, off);
+inline size_t das_smem_bytes_impl(int FB, int NT, int nent_max, int fir_taps, int MIR) {
+  size_t off[9];
+  return layout_bytes(FB, NT, nent_max, (fir_taps - 1) / 2, MIR, off);
 }
 
 template <int FB, int NT, bool T0, int MIR>
 cudaError_t launch_k(const CUtensorMap& tm, const DasArgs& a, const RawMaps& maps, cudaStream_t st) {
-  const size_t smem = das_smem_bytes_impl(FB * MIR, NT, a.entries_per_group, a.fir_taps);
+  const size_t smem = das_smem_bytes_impl(FB * MIR, NT, a.entries_per_group, a.fir_taps, MIR);
   auto kern = das_fused_kernel<FB, NT, T0, MIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -167,6 +167,8 @@ supra_status validate(const supra_bf_config* c) {
   if (c->abi_version != SUPRA_BF_ABI_VERSION)
     return fail(SUPRA_E_PARAM, "abi_version %d != %d", c->abi_version, SUPRA_BF_ABI_VERSION);
   if (c->elements_x < 1 || c->elements_y < 1) return fail(SUPRA_E_PARAM, "elements must be >= 1");
+  if ((int64_t)c->elements_x * c->elements_y > 65535 || c->num_channels > 65535)
+    return fail(SUPRA_E_PARAM, "at most 65535 elements and channels per event");
   if (!(c->pitch_x_mm > 0) || !(c->pitch_y_mm > 0)) return fail(SUPRA_E_PARAM, "pitch must be > 0");
   if (!(c->center_frequency_hz > 0)) return fail(SUPRA_E_PARAM, "center_frequency must be > 0");
   if (c->num_events < 1) return fail(SUPRA_E_PARAM, "num_events must be >= 1");

@@ -222,7 +222,7 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps, int mir
 // (das_warp.cu); same tensor map as launch_das for that shape.
 bool das_warp_ok(int fb, int S, float t0fs);
 cudaError_t launch_das_warp(const CUtensorMap& raw_map, const DasArgs& a, cudaStream_t st);
-size_t das_smem_bytes(int fb, int nt, int nent_max, int fir_taps);
+size_t das_smem_bytes(int fb, int nt, int nent_max, int fir_taps, int mir);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaStream_t st);
