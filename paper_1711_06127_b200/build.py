@@ -13,10 +13,17 @@ OUT = os.path.join(HERE, "libsupra_bf.so")
 BUILD = os.path.join(HERE, "_build")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = (["das.cu"] + [f"das_inst{i}.cu" for i in range(10)] + ["das_warp.cu"] +
-      [f"das_warp_inst{i}.cu" for i in range(3)] + ["epilogue.cu", "scanconv.cu"])
+CU = (["das.cu", "das_warp.cu"] + [f"das_warp_inst{i}.cu" for i in range(3)] + ["epilogue.cu", "scanconv.cu"])
 CPP = ["host.cpp"]
 HDRS = ["internal.h", "epilogue.cuh", "das_common.cuh", "das_kernel.cuh", "das_warp_kernel.cuh"]
+
+
+def das_instances() -> int:
+    """Rows of kDasInst in csrc/das_inst.cu (one DAS kernel per translation unit)."""
+    import re
+    src = open(os.path.join(CSRC, "das_inst.cu")).read()
+    table = src[src.index("kDasInst[][4] = {"):src.index("};", src.index("kDasInst[][4] = {"))]
+    return len(re.findall(r"\{\s*\d+,\s*\d+,\s*[01],\s*\d+\s*\}", table))
 
 
 def _run(cmd, verbose):
@@ -46,18 +53,20 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, var
     hdr_deps = [os.path.join(CSRC, h) for h in HDRS] + [os.path.join(ROOT, "include", "supra_bf.h")]
     objs = []
     cmds = []
-    for f in CU:
+    units = [(f, f + ".o", []) for f in CU]
+    units += [("das_inst.cu", f"das_inst.{i}.o", [f"-DDAS_INST={i}"]) for i in range(das_instances())]
+    for f, o, udefs in units:
         src = os.path.join(CSRC, f)
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(BUILD, o)
         objs.append(obj)
         if force or _stale(obj, [src] + hdr_deps):
-            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, *dflags, "-O3", "-lineinfo", "-std=c++17",
+            cmd = [os.path.join(CUDA, "bin", "nvcc"), *ARCH, *dflags, *udefs, "-O3", "-lineinfo", "-std=c++17",
                    "--expt-relaxed-constexpr", "-Xfatbin=-compress-all", "-Xcompiler", "-fPIC", *inc, "-c", src, "-o", obj]
             if ptxas_v:
                 cmd.insert(1, "-Xptxas=-v")
             cmds.append(cmd)
-    # translation units compile in parallel (the DAS variants are split over
-    # das_inst*.cu / das_warp_inst*.cu for this)
+    # translation units compile in parallel (one DAS batch variant per unit;
+    # the warp-split variants are split over das_warp_inst*.cu)
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
         list(ex.map(lambda c: _run(c, verbose), cmds))

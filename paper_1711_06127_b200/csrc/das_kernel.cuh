@@ -58,13 +58,21 @@ struct SmemLayout {
   int2* slot;       // [4] (event, mirror variant) of every line slot
 };
 
+// Layout: the fixed-size control block (mbarriers, release counters, frame
+// maxima, output slots) first, at constant offsets, then the ring (which
+// doubles as the FIR line buffer), then the per-entry records.  Constant
+// offsets are load immediates and cost no registers in the tap loop.
+constexpr size_t kCtlFull = 0, kCtlRel = 64, kCtlSmax = 96, kCtlVout = 160, kCtlSlot = 288, kCtlBytes = 384;
+static_assert(kMaxStages * 8 <= kCtlRel && kCtlRel + kMaxStages * 4 <= kCtlSmax && kCtlSmax + 16 * 4 <= kCtlVout &&
+                  kCtlVout + 16 * 8 <= kCtlSlot && kCtlSlot + 4 * 8 <= kCtlBytes,
+              "DAS control block layout");
+
 // Bytes of everything except the ring; ring stages fill the rest of the
 // per-CTA budget (2 CTAs per SM), between 3 and kMaxStages.
 __host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P, int MIR) {
-  return align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
+  return kCtlBytes + align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
          (MIR > 1 ? align128(sizeof(uint2) * nent_max) : 0) +
-         align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1)) + align128(sizeof(uint64_t) * kMaxStages) +
-         align128(sizeof(unsigned) * kMaxStages) + align128(sizeof(unsigned) * 16) + align128(sizeof(int2) * 20);
+         align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
 }
 // CTAs per SM: 3 for short passes (NT = 2: 32 accumulators, <= 85
 // registers), else 2; the per-CTA shared-memory budget follows.
@@ -82,15 +90,11 @@ __host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P, i
 __host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int P, int MIR, size_t* off) {
   const size_t ring = (size_t)das_stages(FB, NT, nent_max, P, MIR) * stage_bytes(FB, das_rows_nt(NT));
   const size_t fb = align128((size_t)fir_groups(FB) * fir_span(NT * kTileK, P) * 16);
-  size_t o = 0;
+  size_t o = kCtlBytes;
   off[0] = o; o = align128(o + (ring > fb ? ring : fb));
   off[1] = o; o = align128(o + sizeof(float4) * nent_max);
   off[2] = o; o = align128(o + sizeof(int2) * nent_max);
   off[3] = o; o = align128(o + sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
-  off[4] = o; o = align128(o + sizeof(uint64_t) * kMaxStages);
-  off[5] = o; o = align128(o + sizeof(unsigned) * kMaxStages);
-  off[6] = o; o = align128(o + sizeof(unsigned) * 16);
-  off[7] = o; o = align128(o + sizeof(int2) * 20);
   off[8] = o; o = MIR > 1 ? align128(o + sizeof(uint2) * nent_max) : o;
   return o;
 }
@@ -104,11 +108,11 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT,
   L.rec = (float4*)(base + off[1]);
   L.wse = (int2*)(base + off[2]);
   L.carry = (float4*)(base + off[3]);
-  L.full = (uint64_t*)(base + off[4]);
-  L.rel = (unsigned*)(base + off[5]);
-  L.smax = (unsigned*)(base + off[6]);
-  L.vout = (int2*)(base + off[7]);
-  L.slot = L.vout + 16;
+  L.full = (uint64_t*)(base + kCtlFull);
+  L.rel = (unsigned*)(base + kCtlRel);
+  L.smax = (unsigned*)(base + kCtlSmax);
+  L.vout = (int2*)(base + kCtlVout);
+  L.slot = (int2*)(base + kCtlSlot);
   L.chx = (uint2*)(base + off[8]);
   return L;
 }
