@@ -79,7 +79,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, var
                   "-Wall", "-I", os.path.join(CUDA, "include"), *inc, "-c", src, "-o", obj], verbose)
     if force or _stale(OUT, objs):
         _run([os.path.join(CUDA, "bin", "nvcc"), *ARCH, "-shared", "-o", OUT, *objs,
-              "-Xcompiler", "-fPIC", "-cudart", "static"], verbose)
+              "-Xcompiler", "-fPIC", "-cudart", "static", "-Xlinker", "--no-undefined"], verbose)
     return OUT
 
 

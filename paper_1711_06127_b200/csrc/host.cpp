@@ -675,15 +675,16 @@ supra_status build_sc_tables(supra_bf* h) {
     const bool is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
     const double fovx = c.fov_x_deg * kPi / 180.0, fovy = c.fov_y_deg * kPi / 180.0;
     const double dthx = fovx / (Lx - 1), dthy = is3d ? fovy / (Ly - 1) : 1.0;
-    h->h_rows.assign((size_t)nz * ny, ScRow{0, 0, 0});
+    h->h_rows.assign((size_t)nz * ny, ScRow{0, 0, 0, 0.f});
     h->h_ent.clear();
     std::vector<ScEntry> rowbuf(nx);
-    std::vector<char> okbuf(nx);
+    auto unorm16 = [](double f) { return (uint32_t)std::lrint(std::min(1.0, std::max(0.0, f)) * 65535.0); };
     for (int iz = 0; iz < nz; iz++) {
       const double Z = c.out_origin_mm[2] + iz * c.out_spacing_mm[2];
       for (int iy = 0; iy < ny; iy++) {
         const double Y = c.out_origin_mm[1] + iy * c.out_spacing_mm[1];
         int lo = -1, hi = -1;
+        double fy_row = 0.0;
         for (int ix = 0; ix < nx; ix++) {
           const double X = c.out_origin_mm[0] + ix * c.out_spacing_mm[0];
           double ux, uy = 0.0, v;
@@ -702,20 +703,22 @@ supra_status build_sc_tables(supra_bf* h) {
           sc_axis(ux, Lx, &i0x, &fx);
           sc_axis(uy, is3d ? Ly : 1, &i0y, &fy);
           sc_axis(v, S, &k0, &fz);
-          okbuf[ix] = ok;
-          rowbuf[ix] = ScEntry{ok ? (i0y * Lx + i0x) * S + k0 : -1, (float)fx, (float)fy, (float)fz};
+          rowbuf[ix] = ScEntry{ok ? (uint32_t)((i0y * Lx + i0x) * S + k0) : kScInvalid,
+                               unorm16(fx) | (unorm16(fz) << 16)};
           if (ok) {
             if (lo < 0) lo = ix;
             hi = ix + 1;
             nvalid++;
+            fy_row = fy;  // u_y depends on (Y, Z) only: one value per row
           }
         }
         ScRow& r = h->h_rows[(size_t)iz * ny + iy];
+        if (h->h_ent.size() + nx > 0xFFFFFFFFull) return fail(SUPRA_E_RESOURCE, "scan-conversion table too large");
         if (lo >= 0) {
-          r = ScRow{lo, hi, (int64_t)h->h_ent.size()};
+          r = ScRow{lo, hi, (uint32_t)h->h_ent.size(), (float)fy_row};
           h->h_ent.insert(h->h_ent.end(), rowbuf.begin() + lo, rowbuf.begin() + hi);
         } else {
-          r = ScRow{0, 0, (int64_t)h->h_ent.size()};
+          r = ScRow{0, 0, (uint32_t)h->h_ent.size(), 0.f};
         }
       }
     }
@@ -1275,7 +1278,8 @@ static supra_status run_sc(supra_bf_t h, const void* line_img, int in_type, cons
     }
   }
   if (c.sc_kind == SUPRA_SC_LINEAR_2D) return check_launch(launch_sc_linear(a, sm, st), "sc_linear kernel");
-  return check_launch(launch_sc_table(a, st), "sc_table kernel");
+  const int lbytes = (int)std::min<int64_t>(INT32_MAX, (int64_t)h->L * h->Sd * (in_type == SUPRA_T_U8 ? 1 : 4));
+  return check_launch(launch_sc_table(a, lbytes, st), "sc_table kernel");
 }
 
 supra_status supra_bf_scanconvert(supra_bf_t h, const void* line_img, int32_t frames, void* img, uint8_t* mask,
@@ -1339,11 +1343,11 @@ supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t* valid, int32_t* idx) {
           const ScRow& r = h->h_rows[(size_t)iz * ny + iy];
           valid[n] = 0;
           if (ix >= r.xlo && ix < r.xhi) {
-            int32_t b = h->h_ent[r.off + (ix - r.xlo)].base;
-            if (b >= 0) {
+            const uint32_t b = h->h_ent[r.off + (ix - r.xlo)].base;
+            if (b != kScInvalid) {
               valid[n] = 1;
               idx[3 * n + 2] = b % S;
-              int li = b / S;
+              const int li = (int)(b / S);
               idx[3 * n] = li % Lx;
               idx[3 * n + 1] = li / Lx;
             }

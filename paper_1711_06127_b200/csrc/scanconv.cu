@@ -9,6 +9,7 @@
 //               range and 16-byte entries (corner offset, fx, fy, fz).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -259,48 +260,108 @@ __global__ void __launch_bounds__(256) sc_linear_direct_kernel(const ScArgs a) {
   }
 }
 
-// grid (nz*ny, F); block 256 looping over x.
-__global__ void __launch_bounds__(256) sc_table_kernel(const ScArgs a) {
-  const int r = blockIdx.x, f = blockIdx.y;
-  const float ref = a.frame_max ? __uint_as_float(a.frame_max[f]) : 0.f;
-  const float lref = ref > 0.f ? lg2_approx(ref) : 0.f;
-  auto load_y = [&](const void* p, int type, size_t i) {
-    const float v = ::supra::load_y(p, type, i);
-    return a.frame_max ? y_of_env(v, ref, lref, a.DR_k) : v;
-  };
+// Sector 2D / pyramid 3D: one warp per output row (iz, iy), 8 rows per CTA,
+// and a group of `fpc` frames per CTA.  Lane l takes x = x0 + 32 j + l
+// (j < 4: coalesced 8-byte entry loads and output stores); each entry is
+// read ONCE and applied to every frame of the group (the table, not the
+// L2-resident line image, is the HBM traffic), so a frame costs the gathers,
+// the blend and the output store.  Offsets are 32-bit (L * S < 2^31 and the
+// table < 2^32 entries, checked at create).
+// u32 -> f32 on the full-rate ALU path (I2FP.F32.U32); the compiler's
+// choice for values it knows to be 8/16-bit, I2F.U16, runs at quarter rate.
+__device__ __forceinline__ float u2f(uint32_t x) {
+  float y;
+  asm("cvt.rn.f32.u32 %0, %1;" : "=f"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
+
+// Sector 2D / pyramid 3D: one warp per output row (iz, iy), 8 rows per CTA,
+// and a group of `fpc` frames per CTA.  Lane l takes x = x0 + 32 j + l
+// (j < 4: coalesced 8-byte entry loads and output stores); each entry is
+// read ONCE and applied to every frame of the group, so a frame costs the
+// corner gathers of the L2-resident line image, the blend and the store.
+// Offsets within a frame are 32-bit (L * S < 2^31, checked at create).
+// Measured (C4, u8 line image): bound by the L1 gather path (l1tex data
+// pipe ~70 %, long-scoreboard stalls on the corner loads), not by DRAM;
+// staging each row block's entries in shared memory with bulk copies
+// (double-buffered, persistent CTAs) or z-major warp tiles (4 x by 8 z per
+// warp, ~5 L1 lines per gather instead of ~15) were both slower
+// (60 vs 52 us per C4 volume).
+template <int IN_T, int OUT_T, bool IS3D, bool LOGLOAD>
+__global__ void __launch_bounds__(256, 4) sc_table_kernel(const ScArgs a, int fpc) {
+  constexpr int V = 4;  // voxels per lane and chunk
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= a.nz * a.ny) return;
+  const int f0 = blockIdx.y * fpc, f1 = min(a.F, f0 + fpc);
   const ScRow row = a.rows[r];
-  const size_t S = (size_t)a.S, LS = (size_t)a.Lx * a.S;
-  const size_t fbase = (size_t)f * a.Ly * LS;
-  const size_t obase = ((size_t)f * a.nz * a.ny + r) * a.nx;
-  for (int ix = threadIdx.x; ix < a.nx; ix += blockDim.x) {
-    float v = 0.f;
-    bool ok = false;
-    if (ix >= row.xlo && ix < row.xhi) {
-      const ScEntry e = a.ent[row.off + (ix - row.xlo)];
-      if (e.base >= 0) {
-        ok = true;
-        const size_t b = fbase + (size_t)e.base;
-        const float fx = e.fx, fz = e.fz;
-        const float y000 = load_y(a.line_img, a.in_type, b);
-        const float y001 = load_y(a.line_img, a.in_type, b + 1);
-        const float y100 = load_y(a.line_img, a.in_type, b + S);
-        const float y101 = load_y(a.line_img, a.in_type, b + S + 1);
-        float v0 = (1.f - fz) * ((1.f - fx) * y000 + fx * y100) + fz * ((1.f - fx) * y001 + fx * y101);
-        if (a.is3d) {
-          const float fy = e.fy;
-          const float y010 = load_y(a.line_img, a.in_type, b + LS);
-          const float y011 = load_y(a.line_img, a.in_type, b + LS + 1);
-          const float y110 = load_y(a.line_img, a.in_type, b + LS + S);
-          const float y111 = load_y(a.line_img, a.in_type, b + LS + S + 1);
-          float v1 = (1.f - fz) * ((1.f - fx) * y010 + fx * y110) + fz * ((1.f - fx) * y011 + fx * y111);
-          v = (1.f - fy) * v0 + fy * v1;
-        } else {
-          v = v0;
+  const uint32_t S = (uint32_t)a.S, LS = (uint32_t)a.Lx * S;
+  const size_t fstride = (size_t)a.Ly * LS;  // line-image elements per frame
+  const size_t ostride = (size_t)a.nz * a.ny * a.nx;
+  const float fy = row.fy;
+  using InT = typename std::conditional<IN_T == SUPRA_T_U8, uint8_t, float>::type;
+  // u8 line images are blended as integers 0..255 (exact in f32) and scaled
+  // by 1/255 once at the end
+  constexpr float kInScale = IN_T == SUPRA_T_U8 ? 1.0f / 255.0f : 1.0f;
+  const uint2* rent = reinterpret_cast<const uint2*>(a.ent) + row.off - row.xlo;  // entry of column x: rent[x]
+  for (int x0 = 0; x0 < a.nx; x0 += 32 * V) {
+    uint32_t base[V];
+    float fx[V], fz[V];
+#pragma unroll
+    for (int j = 0; j < V; j++) {
+      const int x = x0 + 32 * j + lane;
+      base[j] = kScInvalid;
+      uint32_t q = 0u;
+      if (x >= row.xlo && x < row.xhi) {
+        const uint2 e = __ldg(rent + x);
+        base[j] = e.x;
+        q = e.y;
+      }
+      fx[j] = u2f(q & 0xFFFFu) * (1.0f / 65535.0f);
+      fz[j] = u2f(q >> 16) * (1.0f / 65535.0f);
+      if (a.mask && f0 == 0 && x < a.nx) a.mask[(size_t)r * a.nx + x] = base[j] != kScInvalid ? 1 : 0;
+    }
+    for (int f = f0; f < f1; f++) {
+      float ref = 0.f, lref = 0.f;
+      if constexpr (LOGLOAD) {
+        ref = __uint_as_float(a.frame_max[f]);
+        lref = ref > 0.f ? lg2_approx(ref) : 0.f;
+      }
+      const InT* lf = (const InT*)a.line_img + (size_t)f * fstride;
+      auto ld = [&](const InT* p) {
+        float y;
+        if constexpr (IN_T == SUPRA_T_U8) y = u2f(__ldg(p));
+        else y = __ldg(p);
+        if constexpr (LOGLOAD) y = y_of_env(y, ref, lref, a.DR_k);
+        return y;
+      };
+      const size_t ob = (size_t)f * ostride + (size_t)r * a.nx;
+#pragma unroll
+      for (int j = 0; j < V; j++) {
+        const int x = x0 + 32 * j + lane;
+        float v = 0.f;
+        if (base[j] != kScInvalid) {
+          const InT* p0 = lf + base[j];  // corner (i0x, i0y, k0)
+          const InT* p1 = p0 + S;        // (i0x + 1, i0y, k0)
+          const float t0 = lerpf(ld(p0), ld(p0 + 1), fz[j]);
+          const float t1 = lerpf(ld(p1), ld(p1 + 1), fz[j]);
+          v = lerpf(t0, t1, fx[j]);
+          if constexpr (IS3D) {
+            const InT* p2 = p0 + LS;  // (i0x, i0y + 1, k0)
+            const InT* p3 = p2 + S;
+            const float t2 = lerpf(ld(p2), ld(p2 + 1), fz[j]);
+            const float t3 = lerpf(ld(p3), ld(p3 + 1), fz[j]);
+            v = lerpf(v, lerpf(t2, t3, fx[j]), fy);
+          }
+          v *= kInScale;
+        }
+        if (x < a.nx) {
+          if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = (uint8_t)__float2uint_rd(fmaf(255.f, v, 0.5f));
+          else ((float*)a.img)[ob + x] = v;
         }
       }
     }
-    store_img(a.img, a.out_type, obase + ix, v);
-    if (a.mask && f == 0) a.mask[(size_t)r * a.nx + ix] = ok ? 1 : 0;
   }
 }
 
@@ -325,10 +386,38 @@ cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t launch_sc_table(const ScArgs& a, cudaStream_t st) {
-  dim3 grid(a.nz * a.ny, a.F);
-  sc_table_kernel<<<grid, 256, 0, st>>>(a);
+template <int IN_T, int OUT_T, bool IS3D, bool LG>
+static cudaError_t launch_tab(const ScArgs& a, int line_img_bytes_per_frame, cudaStream_t st) {
+  // frames per CTA: every table entry is read once per group while the
+  // group's line images stay L2-resident (<= 48 MB of the 126 MB L2); the
+  // grid keeps >= 2 waves of 4 CTAs per SM
+  const long tiles = ((long)a.nz * a.ny + 7) / 8;
+  const long cap = std::max<long>(1, (48L << 20) / std::max(1, line_img_bytes_per_frame));
+  const long fill = std::max<long>(1, tiles * a.F / (148L * 4 * 2));
+  const int fpc = (int)std::min<long>({(long)a.F, cap, fill, 16L});
+  dim3 grid((unsigned)tiles, (a.F + fpc - 1) / fpc);
+  sc_table_kernel<IN_T, OUT_T, IS3D, LG><<<grid, 256, 0, st>>>(a, fpc);
   return cudaGetLastError();
+}
+
+template <int IN_T, int OUT_T, bool IS3D>
+static cudaError_t launch_tab_lg(const ScArgs& a, int bytes, cudaStream_t st) {
+  return a.frame_max ? launch_tab<IN_T, OUT_T, IS3D, true>(a, bytes, st)
+                     : launch_tab<IN_T, OUT_T, IS3D, false>(a, bytes, st);
+}
+
+cudaError_t launch_sc_table(const ScArgs& a, int bytes, cudaStream_t st) {
+  const bool u8in = a.in_type == SUPRA_T_U8, u8out = a.out_type == SUPRA_T_U8;
+  if (a.is3d) {
+    if (u8in) return u8out ? launch_tab_lg<SUPRA_T_U8, SUPRA_T_U8, true>(a, bytes, st)
+                           : launch_tab_lg<SUPRA_T_U8, SUPRA_T_F32, true>(a, bytes, st);
+    return u8out ? launch_tab_lg<SUPRA_T_F32, SUPRA_T_U8, true>(a, bytes, st)
+                 : launch_tab_lg<SUPRA_T_F32, SUPRA_T_F32, true>(a, bytes, st);
+  }
+  if (u8in) return u8out ? launch_tab_lg<SUPRA_T_U8, SUPRA_T_U8, false>(a, bytes, st)
+                         : launch_tab_lg<SUPRA_T_U8, SUPRA_T_F32, false>(a, bytes, st);
+  return u8out ? launch_tab_lg<SUPRA_T_F32, SUPRA_T_U8, false>(a, bytes, st)
+               : launch_tab_lg<SUPRA_T_F32, SUPRA_T_F32, false>(a, bytes, st);
 }
 
 }  // namespace supra
