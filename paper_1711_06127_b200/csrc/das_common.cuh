@@ -148,10 +148,25 @@ __host__ __device__ inline int fir_groups(int FB) { return (FB + 3) / 4; }
 // bank (frequency compounding) env = sum_b w_b env_b, bands in
 // order (the arithmetic of epilogue.cuh envelope_at, so fused and standalone
 // results agree bitwise).
-template <int B>
+// PC > 0: the half-length P = PC is a compile-time constant with PC % 4 == 0
+// (the 65-tap default, P = 32) and o0 - kbase is a multiple of 4, so every
+// buffer read is a load at a compile-time offset from one base address:
+// fir_pad(b0 + d) = b0 + b0/4 + d + floor(d/4) for b0 % 4 == 0.  PC = 0: P
+// at run time.  Same operations in the same order either way.
+template <int B, int PC = 0>
 __device__ __forceinline__ void band_env(const DasArgs& a, const float4* lineg, int kbase, int o0, int P,
                                          float (&env)[4][4]) {
-  auto X = [&](int k) { return lineg[fir_pad(k - kbase)]; };
+  const int b0 = o0 - kbase;
+  const float4* p0 = lineg + b0 + (b0 >> 2);  // X(o0 + d) = p0[d + (d >> 2)] (PC > 0)
+  auto X = [&](int k) {
+    if constexpr (PC > 0) {
+      const int d = k - o0;
+      return p0[d + (d >> 2)];
+    } else {
+      return lineg[fir_pad(k - kbase)];
+    }
+  };
+  if constexpr (PC > 0) P = PC;
   float4 Lw[4], Rw[4];
 #pragma unroll
   for (int o = 0; o < 4; o++) Lw[o] = Rw[o] = X(o0 + o);
@@ -179,6 +194,9 @@ __device__ __forceinline__ void band_env(const DasArgs& a, const float4* lineg, 
       im[o][0] = __ffma2_rn(sj, sub2(l0, r0), im[o][0]);
       im[o][1] = __ffma2_rn(sj, sub2(l1, r1), im[o][1]);
     }
+    // keeps each step's two loads in place: with compile-time offsets the
+    // compiler would otherwise hoist all 2P of them (and spill)
+    if constexpr (PC > 0) asm volatile("" ::: "memory");
   }
   const float w = a.band_w[B];
 #pragma unroll
@@ -193,15 +211,17 @@ __device__ __forceinline__ void band_env(const DasArgs& a, const float4* lineg, 
 
 // vout[q] = (line, frame) of the group's q-th (virtual) frame, frame < 0:
 // nothing to store (past the call's frames).
-template <int FB>
+// PC: compile-time half-length (see band_env), 0 = run time; the caller
+// picks PC = 32 when fir_taps == 65 and (o0 - kbase) % 4 == 0.
+template <int FB, int PC = 0>
 __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg, int kbase, int o0, int o_end,
                                           const int2* vout, float* bmax) {
   const int P = (a.fir_taps - 1) / 2;
   float env[4][4];
-  band_env<0>(a, lineg, kbase, o0, P, env);
-  if (a.nbands > 1) band_env<1>(a, lineg, kbase, o0, P, env);
-  if (a.nbands > 2) band_env<2>(a, lineg, kbase, o0, P, env);
-  if (a.nbands > 3) band_env<3>(a, lineg, kbase, o0, P, env);
+  band_env<0, PC>(a, lineg, kbase, o0, P, env);
+  if (a.nbands > 1) band_env<1, PC>(a, lineg, kbase, o0, P, env);
+  if (a.nbands > 2) band_env<2, PC>(a, lineg, kbase, o0, P, env);
+  if (a.nbands > 3) band_env<3, PC>(a, lineg, kbase, o0, P, env);
   static_assert(kMaxBands == 4, "band unrolling");
 #pragma unroll
   for (int o = 0; o < 4; o++) {

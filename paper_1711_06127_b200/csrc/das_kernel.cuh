@@ -525,6 +525,8 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
     const int o_begin = k0 == 0 ? 0 : k0 - P;
     const int o_end = kend == S ? S : k0 + PL - P;
     const int nblk = (o_end - o_begin + 3) / 4;
+    // (o_begin - kbase = P or 2P: a multiple of 4 for the 65-tap default)
+    const bool p32 = P == 32;
     for (int it = threadIdx.x; it < ng * nblk; it += blockDim.x) {
       const int q4 = it / nblk, blk = it - q4 * nblk;
       if (q4 != curg) {
@@ -532,7 +534,10 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(con
         curg = q4;
         bmax[0] = bmax[1] = bmax[2] = bmax[3] = 0.f;
       }
-      fir_block<VF>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, sm.vout + 4 * q4, bmax);
+      if (p32)
+        fir_block<VF, 32>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, sm.vout + 4 * q4, bmax);
+      else
+        fir_block<VF>(a, sm.line + (size_t)q4 * span, kbase, o_begin + 4 * blk, o_end, sm.vout + 4 * q4, bmax);
     }
     // RF tail k in [k0 + PL - 2P, k0 + PL) for the next pass's first outputs
     if (kend < S)

@@ -316,8 +316,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
   __syncthreads();
   float bmax[4] = {0.f, 0.f, 0.f, 0.f};
   const int2 vout[1] = {make_int2(line, f0)};
-  for (int it = threadIdx.x; it < S / 4; it += blockDim.x)
-    fir_block<1>(a, lineb, kbase, 4 * it, S, vout, bmax);
+  if (P == 32)  // (4 it - kbase = 4 it + 2P: a multiple of 4)
+    for (int it = threadIdx.x; it < S / 4; it += blockDim.x) fir_block<1, 32>(a, lineb, kbase, 4 * it, S, vout, bmax);
+  else
+    for (int it = threadIdx.x; it < S / 4; it += blockDim.x) fir_block<1>(a, lineb, kbase, 4 * it, S, vout, bmax);
   if (!a.ref_fixed) {
     atomicMax(&smax[0], __float_as_uint(bmax[0]));
     __syncthreads();
