@@ -821,23 +821,40 @@ void fill_log(const supra_bf* h, int& fixed, float& k1, float& k0) {
 
 }  // namespace
 
-// DAS launch shape for `frames` frames: mirror lines per CTA (up to
-// mir_max) as many as the layout's symmetry order gives while the grid keeps
-// >= 2 CTAs per SM, else one line per CTA.
-static DasShape pick_shape(supra_bf* h, int frames, int mir_max) {
+// DAS launch shape for `frames` frames of `nlines` lines.  Frames per CTA:
+// the largest feasible (das_shape; the geometry is shared by more frames --
+// smaller groups measured slower even where they fill the GPU better, e.g.
+// Table-1 shapes at 64 frames FB = 8: 0.85 vs 0.65 ms).  Mirror lines per CTA
+// m <= mir_max: the m with the smallest modelled time -- per CTA and tap the
+// cost is G + vf * C issue slots (G ~ 13: geometry and per-entry
+// bookkeeping, shared by the vf = m x frames virtual frames; C ~ 5: per-frame
+// loads, conversions and FMAs), and the busiest SM runs ceil(CTAs / SMs)
+// of them, a lone CTA at ~1/1.8 of the rate of two (C4p, 512 lines, one
+// volume: m = 1, 2, 4 -> 0.87, 0.55, 0.76 ms, so m = 2).  Results do not
+// depend on the choice (fixed per-sample member order; mirror variants
+// beamform every line as (primary, variant)).
+static DasShape pick_shape(supra_bf* h, int frames, int mir_max, int nlines) {
   const supra_bf_config& c = h->cfg;
   int force = 0;
 #ifdef SUPRA_DEV_KNOBS
   if (const char* ev = std::getenv("SUPRA_BF_MIR")) force = std::atoi(ev);  // A/B measurements only
 #endif
-  for (int m = 4; m >= 2; m /= 2) {
+  DasShape best{0, 0, 1};
+  double tbest = 0.0;
+  for (int m = 4; m >= 1; m /= 2) {
     if (m > mir_max || (force && force != m)) continue;
     const DasShape sh = das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps, m);
     if (sh.fb == 0) continue;
-    const long ncta = (long)(h->L / m) * ((frames + sh.fb / m - 1) / (sh.fb / m));
-    if (force || ncta >= 2L * h->num_sms) return sh;
+    const int fbr = sh.fb / m;
+    const long ncta = (long)(nlines / m) * ((frames + fbr - 1) / fbr);
+    const double per_sm = (double)((ncta + h->num_sms - 1) / h->num_sms);
+    const double t = std::max(per_sm, 1.8) * (13.0 + 5.0 * sh.fb);
+    if (best.fb == 0 || t < tbest) {
+      best = sh;
+      tbest = t;
+    }
   }
-  return das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps, 1);
+  return best.fb ? best : das_shape(h->frames_per_cta, h->S, frames, h->entries_per_group, c.fir_taps, 1);
 }
 
 // Largest mirror order usable for lines [line0, line0 + nlines): the whole
@@ -908,7 +925,7 @@ supra_status supra_bf_create(const supra_bf_config* cfg, supra_bf_t* out) {
   }
   const bool t0zero = (float)(cfg->t0_s * cfg->sample_frequency_hz +
                               (cfg->interpolation == SUPRA_INTERP_NEAREST ? 0.5 : 0.0)) == 0.f;
-  const DasShape sh = pick_shape(h, maxF, t0zero ? h->sym_order : 1);
+  const DasShape sh = pick_shape(h, maxF, t0zero ? h->sym_order : 1, h->L);
   cudaError_t e = cudaMalloc((void**)&h->d_frame_max, sizeof(unsigned) * maxF);
   // f32 line-domain scratch [maxF][L][S/dec]: the envelope of a frame-max
   // call with a u8 line image, and supra_bf_beamform_bmode's envelope / y
@@ -1024,11 +1041,11 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
-  // Mirror lines per CTA (build_mirror_tables): the largest order the
-  // layout has whose grid still fills the GPU (>= 2 CTAs per SM); results
-  // do not depend on the choice.  Whole-volume calls with t0 = 0 only.
+  // Mirror lines and frames per CTA (build_mirror_tables, pick_shape):
+  // results do not depend on the choice.  Mirror lines for whole-volume
+  // calls with t0 = 0 only.
   const int mmax = mirror_max(h, line0, nlines, a.t0fs);
-  const DasShape sh = pick_shape(h, frames, mmax);
+  const DasShape sh = pick_shape(h, frames, mmax, nlines);
   const int fbr = sh.fb / sh.mir;  // frames per CTA
   a.cta = h->d_cta[sh.mir == 4 ? 2 : (sh.mir == 2 ? 1 : 0)];
   a.cta_base = line0 / sh.mir;
@@ -1037,7 +1054,7 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
   // that fills the SMs the first grid's tail leaves idle.
   const int Fmain = (frames / fbr) * fbr;
   const int rem = frames - Fmain;
-  const DasShape sh2 = rem ? pick_shape(h, rem, mmax) : sh;
+  const DasShape sh2 = rem ? pick_shape(h, rem, mmax, nlines) : sh;
   const int fbr2 = sh2.fb / sh2.mir;
   const size_t frame_bytes = (size_t)h->E * h->C * h->S * sizeof(int16_t);
   CUtensorMap tm, tm2;
