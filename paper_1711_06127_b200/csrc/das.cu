@@ -42,6 +42,7 @@ extern template cudaError_t launch_k<1, 16, false, 4>(const CUtensorMap&, const 
 extern template cudaError_t launch_k<2, 4, false, 4>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 extern template cudaError_t launch_k<2, 8, false, 4>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 extern template cudaError_t launch_k<4, 4, false, 4>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
+extern template cudaError_t launch_k<1, 4, false, 4>(const CUtensorMap&, const DasArgs&, const RawMaps&, cudaStream_t);
 
 size_t das_smem_bytes(int FB, int NT, int nent_max, int fir_taps, int mir) {
   return das_smem_bytes_impl(FB, NT, nent_max, fir_taps, mir);
@@ -56,25 +57,31 @@ DasShape das_shape(int fb_max, int S, int F, int nent_max, int fir_taps, int mir
   static const int cand1[][2] = {{16, 4}, {8, 8}, {8, 4}, {4, 16}, {4, 8}, {4, 4}, {2, 16},
                                  {2, 8},  {2, 4}, {1, 16}, {1, 8}, {1, 4}};
   static const int cand2[][2] = {{16, 4}, {4, 16}, {4, 8}, {2, 16}, {2, 8}};
-  static const int cand4[][2] = {{16, 4}, {8, 8}, {8, 4}, {4, 16}, {4, 8}};
+  static const int cand4[][2] = {{16, 4}, {8, 8}, {8, 4}, {4, 16}, {4, 8}, {4, 4}};
   const int(*cand)[2] = mir == 4 ? cand4 : (mir == 2 ? cand2 : cand1);
-  const int ncand = mir == 4 ? 5 : (mir == 2 ? 5 : 12);
+  const int ncand = mir == 4 ? 6 : (mir == 2 ? 5 : 12);
   const int ntmax = das_nt(S);
   const int P = (fir_taps - 1) / 2;
   int ofb = 0, ont = 0;
 #ifdef SUPRA_DEV_KNOBS
-  // dev override (A/B measurements only): SUPRA_BF_SHAPE=<fb>x<nt> (mir = 1)
-  if (const char* ev = std::getenv("SUPRA_BF_SHAPE")) std::sscanf(ev, "%dx%d", &ofb, &ont);
+  // dev override (A/B measurements only): SUPRA_BF_SHAPE=<vf>x<nt> for
+  // mir = 1, SUPRA_BF_MIRSHAPE=<vf>x<nt> for mir > 1 (a listed candidate)
+  if (const char* ev = std::getenv(mir == 1 ? "SUPRA_BF_SHAPE" : "SUPRA_BF_MIRSHAPE"))
+    std::sscanf(ev, "%dx%d", &ofb, &ont);
 #endif
   for (int ci = -1; ci < ncand; ci++) {
     const int vf = ci < 0 ? ofb : cand[ci][0], nt = ci < 0 ? ont : cand[ci][1];
-    if (ci < 0 && (mir != 1 || !((vf == 16 && nt == 4) || (vf == 8 && (nt == 4 || nt == 8))))) continue;
+    if (ci < 0) {  // the override must be one of the instantiated candidates
+      bool listed = false;
+      for (int j = 0; j < ncand; j++) listed = listed || (cand[j][0] == ofb && cand[j][1] == ont);
+      if (!listed) continue;
+    }
     const int fb = vf / mir;
     if (fb > fb_max || (fb > F && fb > 1) || nt > ntmax) continue;
     const size_t fixed = fixed_bytes(vf, nent_max, P, mir);
     const size_t ring = 3 * stage_bytes(vf, das_rows_nt(nt));
     const size_t fir = align128((size_t)fir_groups(vf) * fir_span(nt * kTileK, P) * 16);
-    if (fixed + (ring > fir ? ring : fir) > das_smem_budget(nt)) continue;
+    if (fixed + (ring > fir ? ring : fir) > das_smem_budget(vf, nt)) continue;
     return DasShape{vf, nt, mir};
   }
   return mir == 1 ? DasShape{1, 4, 1} : DasShape{0, 0, mir};  // {0, ...}: no feasible mirror shape
@@ -110,6 +117,7 @@ static cudaError_t launch_mir(const CUtensorMap& tm, const DasArgs& a, const Raw
   }
   if (fb == 4) return launch_k<4, 4, false, 4>(tm, a, m, st);
   if (fb == 2) return nt == 4 ? launch_k<2, 4, false, 4>(tm, a, m, st) : launch_k<2, 8, false, 4>(tm, a, m, st);
+  if (nt == 4) return launch_k<1, 4, false, 4>(tm, a, m, st);
   return nt == 8 ? launch_k<1, 8, false, 4>(tm, a, m, st) : launch_k<1, 16, false, 4>(tm, a, m, st);
 }
 

@@ -44,6 +44,7 @@ constexpr int kDasInst[][4] = {
     {2, 4, 0, 4},  // 31
     {2, 8, 0, 4},  // 32
     {4, 4, 0, 4},  // 33
+    {1, 4, 0, 4},  // 34
 };
 #ifdef DAS_INST
 template cudaError_t launch_k<kDasInst[DAS_INST][0], kDasInst[DAS_INST][1], kDasInst[DAS_INST][2] != 0,

@@ -74,15 +74,18 @@ __host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P, int M
          (MIR > 1 ? align128(sizeof(uint2) * nent_max) : 0) +
          align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
 }
-// CTAs per SM: 3 for short passes (NT = 2: 32 accumulators, <= 85
-// registers), else 2; the per-CTA shared-memory budget follows.
-__host__ __device__ constexpr int das_ctas_per_sm(int NT) { return NT == 2 ? 3 : 2; }
-__host__ __device__ constexpr size_t das_smem_budget(int NT) { return NT == 2 ? 75 * 1024 : 113 * 1024; }
+// CTAs per SM: 3 for short passes (NT = 2: <= 85 registers), else 2 (128
+// registers; at 85 the 16-accumulator shapes <4,4> and <1,4,MIR=4> spill
+// 640 bytes); the per-CTA shared-memory budget follows.
+__host__ __device__ constexpr int das_ctas_per_sm(int VF, int NT) { return NT == 2 ? 3 : 2; }
+__host__ __device__ constexpr size_t das_smem_budget(int VF, int NT) {
+  return das_ctas_per_sm(VF, NT) == 3 ? 75 * 1024 : 113 * 1024;
+}
 
 __host__ __device__ inline int das_stages(int FB, int NT, int nent_max, int P, int MIR) {
   const size_t fixed = fixed_bytes(FB, nent_max, P, MIR);
   const size_t sb = stage_bytes(FB, das_rows_nt(NT));
-  const size_t budget = das_smem_budget(NT);
+  const size_t budget = das_smem_budget(FB, NT);
   const long n = fixed >= budget ? 0 : (long)((budget - fixed) / sb);
   return n < 3 ? 3 : (n > kMaxStages ? kMaxStages : (int)n);
 }
@@ -288,7 +291,7 @@ __device__ __forceinline__ void dispatch_tiles(int g, const DasArgs& a, const fl
 // windows [v][rows][32] (one TMA per slot, FB frames each), and the tap
 // geometry computed for the primary line is applied to all VF.
 template <int FB, int NT, bool T0, int MIR>
-__global__ void __launch_bounds__(256, das_ctas_per_sm(NT)) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const DasArgs a,
                                                           const __grid_constant__ RawMaps rmaps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
