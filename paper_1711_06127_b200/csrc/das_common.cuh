@@ -223,6 +223,37 @@ __device__ __forceinline__ void fir_block(const DasArgs& a, const float4* lineg,
   if (a.nbands > 2) band_env<2, PC>(a, lineg, kbase, o0, P, env);
   if (a.nbands > 3) band_env<3, PC>(a, lineg, kbase, o0, P, env);
   static_assert(kMaxBands == 4, "band unrolling");
+  if (a.vec_out && a.dec == 1 && o0 + 3 < o_end) {
+    // the 4 outputs are consecutive samples of each frame's line: one
+    // 16-byte (f32) or 4-byte (u8) store per frame (o0 % 4 == 0, S % 32 == 0)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      if (q >= FB) break;
+      const int2 lf = vout[q];
+      if (lf.y < 0) continue;
+      const size_t base = ((size_t)lf.y * a.L + lf.x) * a.Sd + o0;
+      if (a.ref_fixed) {
+        float y[4];
+#pragma unroll
+        for (int o = 0; o < 4; o++) {
+          const float e = env[o][q];
+          y[o] = e > 0.f ? fminf(fmaxf(fmaf(a.log_k1, lg2_approx(e), a.log_k0), 0.f), 1.f) : 0.f;
+        }
+        if (a.y_type == SUPRA_T_U8) {
+          uint32_t w = 0u;
+#pragma unroll
+          for (int o = 0; o < 4; o++) w |= (uint32_t)(uint8_t)floorf(255.f * y[o] + 0.5f) << (8 * o);
+          *reinterpret_cast<uint32_t*>((uint8_t*)a.y_out + base) = w;
+        } else {
+          *reinterpret_cast<float4*>((float*)a.y_out + base) = make_float4(y[0], y[1], y[2], y[3]);
+        }
+      } else {
+        *reinterpret_cast<float4*>(a.env_out + base) = make_float4(env[0][q], env[1][q], env[2][q], env[3][q]);
+        bmax[q] = fmaxf(bmax[q], fmaxf(fmaxf(env[0][q], env[1][q]), fmaxf(env[2][q], env[3][q])));
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int o = 0; o < 4; o++) {
     const int k = o0 + o;

@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
         }
       }
     };
-    if (threadIdx.x == 0 && a.debug_skip != 2) {
+    if (threadIdx.x == 0 && SUPRA_DBG(a) != 2) {
       // the ring was last written through the generic proxy (line buffer)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       for (int jj = 0, b = buf; jj < NS && jj < np; jj++, b = (b + 1 == NS ? 0 : b + 1)) produce(jj, b);
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
     acc.zero();
     const float kt0f = (float)(k0 + kt);
     for (int j = 0; j < np; j++) {
-      if (a.debug_skip != 2) mbar_wait(&sm.full[buf], phase);
+      if (SUPRA_DBG(a) != 2) mbar_wait(&sm.full[buf], phase);
       const float4 r = sm.rec[j];
       const int kenter = __float_as_int(r.w);
       const int wsm = sm.wse[j].x + kFloorMagicBits - k0 - kt;
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
       // are < k_enter are skipped.
       int m0 = kenter - k0 - kwarp_last;
       m0 = m0 <= 0 ? 0 : (m0 + kTileK - 1) / kTileK;
-      if (a.debug_skip != 1 && m0 < NT)
+      if (SUPRA_DBG(a) != 1 && m0 < NT)
         dispatch_tiles<VF, NT, T0>(m0 / tile_gran(NT), a, r, kenter, wsm, st, kt, k0, kt0f, acc);
       // release the slot; the last warp to release it refills it (no warp
       // ever waits for another to issue a copy)
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
         const unsigned prev = atom_add_acqrel(&sm.rel[buf], 1u);
         if (prev == (blockDim.x / 32) - 1) {
           sm.rel[buf] = 0u;
-          if (j + NS < np && a.debug_skip != 2) {
+          if (j + NS < np && SUPRA_DBG(a) != 2) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             produce(j + NS, buf);
           }

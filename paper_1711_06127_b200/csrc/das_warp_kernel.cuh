@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     mbar_arrive_tx(bar, (unsigned)(ROWS * kRowSamples * 2));
     tma_load_5d(ring + (size_t)(warp * NSW + slot) * SB, &tmap, 0, ws / kRowSamples, ech[j * 4 + var], ev, fm, bar);
   };
-  if (lane == 0 && a.debug_skip != 2)
+  if (lane == 0 && SUPRA_DBG(a) != 2)
     for (int s = 0; s < NSW; s++)
       if (warp + kWarps * s < np) produce(warp + kWarps * s, s);
 
@@ -260,15 +260,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) das_warp_kernel(const __
     c.wsl = ws + kFloorMagicBits - lane;
     c.sbase = smem_u32(ring + (size_t)(warp * NSW + slot) * SB);
     c.abase = c.sbase - 2u * (uint32_t)c.wsl;
-    if (a.debug_skip != 2) mbar_wait(&full[warp * kMaxWarpStages + slot], phase);
+    if (SUPRA_DBG(a) != 2) mbar_wait(&full[warp * kMaxWarpStages + slot], phase);
     // opaque per-entry copy of the lane coordinate: keeps the compiler from
     // hoisting the 2 NP per-pair (h, h^2) constants out of the entry loop
     // (they would be spilled to local memory)
     float2 lf = lanef;
     asm volatile("" : "+f"(lf.x), "+f"(lf.y));
-    if (a.debug_skip != 1) entry_pairs<NP, HANN, MODE>(e.kenter >> 6, a, c, rkt, lane, lf, acc);
+    if (SUPRA_DBG(a) != 1) entry_pairs<NP, HANN, MODE>(e.kenter >> 6, a, c, rkt, lane, lf, acc);
     __syncwarp();
-    if (lane == 0 && j + kWarps * NSW < np && a.debug_skip != 2) {
+    if (lane == 0 && j + kWarps * NSW < np && SUPRA_DBG(a) != 2) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       produce(j + kWarps * NSW, slot);
     }

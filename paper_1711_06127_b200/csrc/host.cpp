@@ -1041,6 +1041,10 @@ static supra_status run_das(supra_bf_t h, const void* raw, int32_t frames, int l
       if (e != cudaSuccess) return check_launch(e, "memset frame_max");
     }
   }
+  {
+    const void* out = a.ref_fixed ? a.y_out : (const void*)a.env_out;
+    a.vec_out = out != nullptr && ((uintptr_t)out & 15) == 0;
+  }
   // Mirror lines and frames per CTA (build_mirror_tables, pick_shape):
   // results do not depend on the choice.  Mirror lines for whole-volume
   // calls with t0 = 0 only.

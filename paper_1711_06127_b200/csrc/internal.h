@@ -97,6 +97,7 @@ struct DasArgs {
   int y_type;                  // SUPRA_T_F32 / SUPRA_T_U8
   unsigned* frame_max;         // [F] float bits (frame-max mode)
   int debug_skip;              // measurement only: skip the tap loop (TMA pipeline alone)
+  int vec_out;                 // 1: line outputs 16-byte aligned (4 consecutive samples per store)
   // 1: windows use the row-cut tensor maps of the launch's RawMaps kernel
   // parameter (exact windows); 0: every window uses the launch's map
   int row_cut;
@@ -207,6 +208,13 @@ struct ScArgs {
 };
 
 #ifdef __CUDACC__
+// The measurement-only debug modes exist in -DSUPRA_DEV_KNOBS builds only;
+// the product kernels always run the whole path (the checks fold away).
+#ifdef SUPRA_DEV_KNOBS
+#define SUPRA_DBG(a) ((a).debug_skip)
+#else
+#define SUPRA_DBG(a) 0
+#endif
 // log2 via MUFU.LG2: absolute error <= 2^-22.6 (PTX ISA), i.e. <= 1.6e-6 dB
 // after the 20 log10 2 scale -- far inside the 0.01 dB contract.
 __device__ __forceinline__ float lg2_approx(float x) {
