@@ -60,9 +60,17 @@ constexpr int kScWarpLines = kScWarpLinesMax + 1;  // + the zero pair
 template <bool U8OUT>
 __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_constant__ CUtensorMap tm,
                                                               const ScArgs a, int fpc) {
-  __shared__ __align__(128) float slab[2][kScMaxLines * kScMaxK];
-  constexpr int TZS = kScWarpLines + 1;  // odd row stride: conflict-free row writes
-  __shared__ float tzw[8][kScRows * TZS];
+  // the two slab buffers live in dynamic shared memory (the pair buffers
+  // below are static; together they exceed the 48 KB static limit)
+  extern __shared__ __align__(128) float slab_dyn[];
+  // per buffer (as sized by launch_sc_linear); 128-byte aligned TMA destinations
+  const int slab_elems = (a.slab_box_l * max(a.slab_box_k, a.slab_k) + 31) & ~31;
+  auto slab = [&](int b) { return slab_dyn + b * slab_elems; };
+  // per warp and output row: pairs {t(j), t(j+1) - t(j)} of the depth-lerped
+  // lines (u8: t scaled to 255 t + 1/2), so a pixel is one LDS.64 + FFMA;
+  // odd row stride in 8-byte units: conflict-free 64-bit row writes
+  constexpr int TZS = kScWarpLines + 1;
+  __shared__ float2 tzw[8][kScRows * TZS];
   __shared__ ScAxis saz[kScRows];
   __shared__ __align__(8) uint64_t full[2], empty[2];
   const int cb = blockIdx.x, rb = blockIdx.y;
@@ -97,14 +105,12 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
   const unsigned whi = __reduce_max_sync(0xffffffffu, colok ? (unsigned)(ax.i0 - l0 + 1) : 0u);
   const int wl0 = wlo == 0xffffffffu ? 0 : (int)wlo;
   const int wnl = wlo == 0xffffffffu ? 0 : (int)(whi - wlo + 1);  // <= kScWarpLines - 1 (checked at create)
-  float* tz = tzw[warp];
-  // zero pair for invalid columns, and per-column pointers
-  const float* tcol = tz + (colok ? ax.i0 - l0 - wl0 : kScWarpLines - 1);
+  float2* tz = tzw[warp];
+  // zero pair for invalid columns (u8: {1/2, 0} -> floor(1/2) = 0), and
+  // per-column pointers
+  const float2* tcol = tz + (colok ? ax.i0 - l0 - wl0 : kScWarpLines - 1);
   const float fx = colok ? ax.f : 0.f;
-  for (int r = lane; r < kScRows; r += 32) {
-    tz[r * TZS + kScWarpLines - 1] = 0.f;
-    tz[r * TZS + kScWarpLines] = 0.f;
-  }
+  for (int r = lane; r < kScRows; r += 32) tz[r * TZS + kScWarpLines - 1] = make_float2(U8OUT ? 0.5f : 0.f, 0.f);
   __syncthreads();
   auto wait = [](uint64_t* bar, unsigned parity) {
     asm volatile(
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
       if (bytes)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3}], [%4];" ::"r"((uint32_t)__cvta_generic_to_shared(slab[b])),
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"((uint32_t)__cvta_generic_to_shared(slab(b))),
             "l"(reinterpret_cast<uint64_t>(&tm)), "r"(kal), "r"(f * Lx + l0), "r"(bb)
             : "memory");
       return;
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
     for (int l = lane; l < nl && kmin >= 0; l += 32)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              (uint32_t)__cvta_generic_to_shared(slab[b] + l * a.slab_box_k)),
+              (uint32_t)__cvta_generic_to_shared(slab(b) + l * a.slab_box_k)),
           "l"(src + (size_t)(l0 + l) * S + kal), "r"((unsigned)seg * 4u), "r"(bb)
           : "memory");
   };
@@ -160,19 +166,19 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
       }
       wait(&full[b], (unsigned)((it >> 1) & 1));
     } else {
-      if (it > 0) __syncthreads();  // every warp is done with slab[0]
+      if (it > 0) __syncthreads();  // every warp is done with slab(0)
       if (kmin >= 0 && nl > 0) {
         const size_t fbase = (size_t)f * Lx * S;
         if (a.in_type == SUPRA_T_F32) {
           const float* src = (const float*)a.line_img + fbase;
           for (int l = warp; l < nl; l += 8)
             for (int kk = lane; kk < ks; kk += 32)
-              cp_async4(slab[0] + l * ks + kk, src + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
+              cp_async4(slab(0) + l * ks + kk, src + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
           asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
         } else {
           for (int l = warp; l < nl; l += 8)
             for (int kk = lane; kk < ks; kk += 32)
-              slab[0][l * ks + kk] =
+              slab(0)[l * ks + kk] =
                   load_y(a.line_img, a.in_type, fbase + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
         }
       }
@@ -186,18 +192,21 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
       ref = __uint_as_float(a.frame_max[f]);
       lref = ref > 0.f ? lg2_approx(ref) : 0.f;
     }
+    float tprev = 0.f;
     for (int j = 0; j < wnl; j++) {
-      const float* y = slab[b] + (wl0 + j) * kstride - (use_tma ? kal : kmin);
+      const float* y = slab(b) + (wl0 + j) * kstride - (use_tma ? kal : kmin);
+      float t = 0.f;
       if (lane < rows && az.i0 >= 0) {
         float y0 = y[az.i0], y1 = y[az.i0 + 1];
         if (a.frame_max) {
           y0 = y_of_env(y0, ref, lref, a.DR_k);
           y1 = y_of_env(y1, ref, lref, a.DR_k);
         }
-        tz[lane * TZS + j] = fmaf(az.f, y1 - y0, y0);
-      } else if (lane < rows) {
-        tz[lane * TZS + j] = 0.f;
+        t = fmaf(az.f, y1 - y0, y0);
       }
+      if (U8OUT) t = fmaf(255.f, t, 0.5f);
+      if (j > 0 && lane < rows) tz[lane * TZS + j - 1] = make_float2(tprev, t - tprev);
+      tprev = t;
     }
     __syncwarp();
     if (use_tma && lane == 0)
@@ -213,16 +222,15 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
         uint8_t* o = (uint8_t*)a.img + out0;
 #pragma unroll 8
         for (int r = 0; r < rows; r++, o += nx) {
-          const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
-          const float v = fmaf(255.f, fmaf(fx, t1 - t0, t0), 0.5f);
-          *o = (uint8_t)__float_as_uint(__fadd_rd(v, 12582912.0f));
+          const float2 t = tcol[r * TZS];  // {255 t0 + 1/2, 255 (t1 - t0)}
+          *o = (uint8_t)__float_as_uint(__fadd_rd(fmaf(fx, t.y, t.x), 12582912.0f));
         }
       } else {
         float* o = (float*)a.img + out0;
 #pragma unroll 8
         for (int r = 0; r < rows; r++, o += nx) {
-          const float t0 = tcol[r * TZS], t1 = tcol[r * TZS + 1];
-          *o = fmaf(fx, t1 - t0, t0);
+          const float2 t = tcol[r * TZS];  // {t0, t1 - t0}
+          *o = fmaf(fx, t.y, t.x);
         }
       }
       if (a.mask && f == 0)
@@ -381,8 +389,14 @@ cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaS
   dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, (a.F + fpc - 1) / fpc);
   CUtensorMap none{};
   const CUtensorMap& tm = slab_map ? *slab_map : none;
-  if (a.out_type == SUPRA_T_U8) sc_linear_tiled_kernel<true><<<grid, 256, 0, st>>>(tm, a, fpc);
-  else sc_linear_tiled_kernel<false><<<grid, 256, 0, st>>>(tm, a, fpc);
+  const size_t smem = 2 * (size_t)((a.slab_box_l * std::max(a.slab_box_k, a.slab_k) + 31) & ~31) * sizeof(float);
+  if (a.out_type == SUPRA_T_U8) {
+    cudaFuncSetAttribute(sc_linear_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sc_linear_tiled_kernel<true><<<grid, 256, smem, st>>>(tm, a, fpc);
+  } else {
+    cudaFuncSetAttribute(sc_linear_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sc_linear_tiled_kernel<false><<<grid, 256, smem, st>>>(tm, a, fpc);
+  }
   return cudaGetLastError();
 }
 
