@@ -47,9 +47,8 @@ __device__ __forceinline__ int sel4(int4 v, int i) { return i == 0 ? v.x : (i ==
 struct SmemLayout {
   int16_t* stage;   // [NS][stage_bytes]
   float4* line;     // FIR line buffer, aliases the stage ring between passes
-  float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter bits}
-  int2* wse;        // [nent] {window start ws, slot-0 channel | rcut << 20}
-  uint2* chx;       // [nent] (MIR > 1) channels of slots 0..3, 16 bits each
+  float4* rec;      // [nent] {|q|^2/2, d.q, pi*cu, k_enter | (ws/32 + 1) << 13 | rcut << 21}
+  uint2* chx;       // [nent] channels of line slots 0..3, 16 bits each
   float4* carry;    // [ngroups][2P] RF tail of the previous pass
   uint64_t* full;   // [kMaxStages]
   unsigned* rel;    // [kMaxStages] warps done with the slot (last one refills it)
@@ -70,8 +69,7 @@ static_assert(kMaxStages * 8 <= kCtlRel && kCtlRel + kMaxStages * 4 <= kCtlSmax 
 // Bytes of everything except the ring; ring stages fill the rest of the
 // per-CTA budget (2 CTAs per SM), between 3 and kMaxStages.
 __host__ __device__ inline size_t fixed_bytes(int FB, int nent_max, int P, int MIR) {
-  return kCtlBytes + align128(sizeof(float4) * nent_max) + align128(sizeof(int2) * nent_max) +
-         (MIR > 1 ? align128(sizeof(uint2) * nent_max) : 0) +
+  return kCtlBytes + align128(sizeof(float4) * nent_max) + align128(sizeof(uint2) * nent_max) +
          align128(sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
 }
 // CTAs per SM: 3 for short passes (NT = 2: <= 85 registers), else 2 (128
@@ -96,9 +94,8 @@ __host__ __device__ inline size_t layout_bytes(int FB, int NT, int nent_max, int
   size_t o = kCtlBytes;
   off[0] = o; o = align128(o + (ring > fb ? ring : fb));
   off[1] = o; o = align128(o + sizeof(float4) * nent_max);
-  off[2] = o; o = align128(o + sizeof(int2) * nent_max);
+  off[2] = o; o = align128(o + sizeof(uint2) * nent_max);
   off[3] = o; o = align128(o + sizeof(float4) * fir_groups(FB) * 2 * (P > 0 ? P : 1));
-  off[8] = o; o = MIR > 1 ? align128(o + sizeof(uint2) * nent_max) : o;
   return o;
 }
 
@@ -109,14 +106,13 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* base, int FB, int NT,
   L.stage = (int16_t*)(base + off[0]);
   L.line = (float4*)(base + off[0]);
   L.rec = (float4*)(base + off[1]);
-  L.wse = (int2*)(base + off[2]);
+  L.chx = (uint2*)(base + off[2]);
   L.carry = (float4*)(base + off[3]);
   L.full = (uint64_t*)(base + kCtlFull);
   L.rel = (unsigned*)(base + kCtlRel);
   L.smax = (unsigned*)(base + kCtlSmax);
   L.vout = (int2*)(base + kCtlVout);
   L.slot = (int2*)(base + kCtlSlot);
-  L.chx = (uint2*)(base + off[8]);
   return L;
 }
 
@@ -393,37 +389,34 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
       const float hl = 0.5f * (float)kl;
       const float tl = (float)kl + split_delay(Ah, B, hl, kl > 0 ? hl * hl : 1e-20f) + a.t0fs;
       const int rcut = max(1, min(S / kRowSamples, ((int)floorf(tl) + 3 + kRowSamples - 1) / kRowSamples));
-      sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu, __int_as_float(e.kenter));
+      // k_enter < S <= 4096 (13 bits), ws / 32 + 1 in [0, 129] and rcut in
+      // [1, 128] (8 bits each)
+      sm.rec[i] = make_float4(Ah, B, 3.14159265358979f * e.cu,
+                              __int_as_float(e.kenter | ((ws / kRowSamples + 1) << 13) | (rcut << 21)));
       // channels of the line slots, resolved here (off the refill path:
       // a global load in produce() would sit between a slot's release and
       // its refill)
       const int4 ch4 = *reinterpret_cast<const int4*>(ech + (size_t)ei * 4);
       const int c0 = sel4(ch4, sm.slot[0].y);
-      sm.wse[i] = make_int2(ws, c0 | (rcut << 20));
-      if constexpr (MIR > 1)
-        sm.chx[i] = make_uint2((unsigned)c0 | ((unsigned)sel4(ch4, sm.slot[1].y) << 16),
-                               MIR > 2 ? (unsigned)sel4(ch4, sm.slot[2].y) | ((unsigned)sel4(ch4, sm.slot[3].y) << 16) : 0u);
+      sm.chx[i] = make_uint2((unsigned)c0 | (MIR > 1 ? (unsigned)sel4(ch4, sm.slot[1].y) << 16 : 0u),
+                             MIR > 2 ? (unsigned)sel4(ch4, sm.slot[2].y) | ((unsigned)sel4(ch4, sm.slot[3].y) << 16) : 0u);
     }
     __syncthreads();  // records visible; the previous pass is done with the line buffer
 
     // TMA of entry jj's window (all FB frames) into ring slot `buf`.
     auto produce = [&](int jj, int buf) {
-      const int2 we = sm.wse[jj];
+      const int w = __float_as_int(sm.rec[jj].w);
+      const int wsrow = ((w >> 13) & 0xFF) - 1;
       // rows at or past rcut are out of bounds in rmaps.m[rcut - 1]: zero
       // fill, no DRAM read (the box size, and so the tx count, is fixed)
-      const CUtensorMap* m = a.row_cut ? &rmaps.m[(we.y >> 20) - 1] : &tmap;
+      const CUtensorMap* m = a.row_cut ? &rmaps.m[((w >> 21) & 0xFF) - 1] : &tmap;
       mbar_arrive_tx(&sm.full[buf], (unsigned)(VF * FR * 2));
-      if constexpr (MIR == 1) {
-        tma_load_5d((unsigned char*)sm.stage + buf * SB, m, 0, we.x / kRowSamples, we.y & 0xFFFFF, sm.slot[0].x, fm,
-                    &sm.full[buf]);
-      } else {
-        const uint2 cx = sm.chx[jj];
+      const uint2 cx = sm.chx[jj];
 #pragma unroll
-        for (int s = 0; s < MIR; s++) {  // slot s: its event, its mirrored channel
-          const unsigned w = s < 2 ? cx.x : cx.y;
-          tma_load_5d((unsigned char*)sm.stage + buf * SB + (size_t)s * FB * FR * 2, m, 0, we.x / kRowSamples,
-                      (int)((s & 1) ? w >> 16 : w & 0xFFFFu), sm.slot[s].x, fm, &sm.full[buf]);
-        }
+      for (int s = 0; s < MIR; s++) {  // slot s: its event, its (mirrored) channel
+        const unsigned cw = s < 2 ? cx.x : cx.y;
+        tma_load_5d((unsigned char*)sm.stage + buf * SB + (size_t)s * FB * FR * 2, m, 0, wsrow,
+                    (int)((s & 1) ? cw >> 16 : cw & 0xFFFFu), sm.slot[s].x, fm, &sm.full[buf]);
       }
     };
     if (threadIdx.x == 0 && SUPRA_DBG(a) != 2) {
@@ -438,8 +431,8 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
     for (int j = 0; j < np; j++) {
       if (SUPRA_DBG(a) != 2) mbar_wait(&sm.full[buf], phase);
       const float4 r = sm.rec[j];
-      const int kenter = __float_as_int(r.w);
-      const int wsm = sm.wse[j].x + kFloorMagicBits - k0 - kt;
+      const int kenter = __float_as_int(r.w) & 0x1FFF;
+      const int wsm = (((__float_as_int(r.w) >> 13) & 0xFF) - 1) * kRowSamples + kFloorMagicBits - k0 - kt;
       const unsigned short* st = (const unsigned short*)((const unsigned char*)sm.stage + buf * SB);
       // first tile of the pass in which this WARP has a member sample
       // (warp-uniform): straight-line code from there (the chains of
