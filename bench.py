@@ -382,8 +382,11 @@ def main():
         if world > 1:
             dist.all_reduce(rate, op=dist.ReduceOp.MIN)
         e2e = {"value": float(rate) * world, "unit": "frames/s",
-               "h2d_bytes_per_step": int(raw_h.numel() * 2), "d2h_bytes_per_step": int(img_h.numel()),
-               "frames_per_step": E, "api": "paper_1711_06127_b200.pipeline.HostPipeline"}
+               "h2d_bytes_per_step": int(pipe.h2d_bytes), "d2h_bytes_per_step": int(img_h.numel()),
+               "frames_per_step": E, "api": "paper_1711_06127_b200.pipeline.HostPipeline",
+               "h2d": "supra_bf_stage_raw: the device reads the referenced sample ranges of each "
+                      "pinned host frame over PCIe (%.0f %% of the %d-byte frame)"
+                      % (100.0 * pipe.h2d_bytes / max(1, raw_h.numel() * 2), raw_h[0].numel() * 2)}
 
     cpu_baseline = None
     secondary = None

@@ -314,6 +314,31 @@ supra_status supra_bf_sc_indices(supra_bf_t h, uint8_t *valid, int32_t *idx);
 supra_status supra_bf_info(supra_bf_t h, int64_t *info8);
 
 /*
+ * supra_bf_stage_raw -- host->device input staging for the end-to-end path:
+ * for every frame, event and channel, copy from src to the same positions of
+ * dst only the sample range supra_bf_beamform reads -- the hull of
+ * [floor tau(k_enter), floor tau(S-1) + 1] over the lines and aperture
+ * members that use the trace (reading #6), widened by one
+ * sample and rounded out to 16 bytes.  Samples outside those ranges are
+ * left untouched in dst and are never read by supra_bf_beamform, so
+ * beamforming dst gives exactly the result of beamforming a full copy of
+ * src.  With src in page-locked host memory the device reads it over PCIe:
+ * the transfer carries the referenced bytes only (C2: 41 % of a frame).
+ * Arguments:
+ *   src  : int16 [frames][num_events][channels][samples], 16-byte aligned;
+ *          page-locked host memory (cudaHostAlloc / cudaMallocHost) or
+ *          device memory of cfg.device.
+ *   dst  : device int16, same shape, 16-byte aligned.
+ *   frames : 0 .. max_frames_per_call.
+ *   bytes_per_frame : NULL or host int64, set to the bytes copied per frame.
+ *   stream : cudaStream_t (the copy is asynchronous on it).
+ * Errors: SUPRA_E_STRUCT on a NULL handle/buffer, misalignment, frames out
+ * of range, pageable src, or dst not device memory of cfg.device.
+ */
+supra_status supra_bf_stage_raw(supra_bf_t h, const void *src, void *dst, int32_t frames,
+                                int64_t *bytes_per_frame, void *stream);
+
+/*
  * supra_bf_set_das_events -- measurement hook for the bench: when non-NULL,
  * supra_bf_beamform records `before` and `after` (cudaEvent_t) on its stream
  * immediately around the DAS kernel launch, so the kernel's duration can be

@@ -31,7 +31,7 @@ SC_LINEAR_2D, SC_SECTOR_2D, SC_PYRAMID_3D = 0, 1, 2
 EXPORTS = ("supra_bf_create", "supra_bf_beamform", "supra_bf_envelope_log", "supra_bf_scanconvert",
            "supra_bf_destroy", "supra_bf_last_error", "supra_bf_sc_indices", "supra_bf_info",
            "supra_bf_set_das_events", "supra_bf_beamform_lines", "supra_bf_log_compress",
-           "supra_bf_beamform_bmode")
+           "supra_bf_beamform_bmode", "supra_bf_stage_raw")
 
 
 class SupraError(RuntimeError):
@@ -108,6 +108,8 @@ def lib():
         L.supra_bf_log_compress.restype = C.c_int
         L.supra_bf_beamform_bmode.argtypes = [vp, vp, C.c_int32, vp, vp, vp]
         L.supra_bf_beamform_bmode.restype = C.c_int
+        L.supra_bf_stage_raw.argtypes = [vp, vp, vp, C.c_int32, vp, vp]
+        L.supra_bf_stage_raw.restype = C.c_int
         _lib = L
     return _lib
 
@@ -225,6 +227,13 @@ class SupraBF:
         scan conversion); img as for scanconvert."""
         _check(lib().supra_bf_beamform_bmode(self.h, _ptr(raw), frames, _ptr(img), _ptr(mask),
                                              _stream(stream)))
+
+    def stage_raw(self, src, dst, frames: int, stream=None) -> int:
+        """Copy the referenced sample ranges of src (pinned host or device
+        int16 [F][E][C][S]) into device dst; returns the bytes moved per frame."""
+        n = C.c_int64(0)
+        _check(lib().supra_bf_stage_raw(self.h, _ptr(src), _ptr(dst), frames, C.byref(n), _stream(stream)))
+        return int(n.value)
 
     def scanconvert(self, line_img, frames: int, img, mask=None, stream=None):
         _check(lib().supra_bf_scanconvert(self.h, _ptr(line_img), frames, _ptr(img), _ptr(mask),

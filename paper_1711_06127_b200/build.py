@@ -13,7 +13,8 @@ OUT = os.path.join(HERE, "libsupra_bf.so")
 BUILD = os.path.join(HERE, "_build")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = (["das.cu", "das_warp.cu"] + [f"das_warp_inst{i}.cu" for i in range(3)] + ["epilogue.cu", "scanconv.cu"])
+CU = (["das.cu", "das_warp.cu"] + [f"das_warp_inst{i}.cu" for i in range(3)] +
+      ["epilogue.cu", "scanconv.cu", "stage.cu"])
 CPP = ["host.cpp"]
 HDRS = ["internal.h", "epilogue.cuh", "das_common.cuh", "das_kernel.cuh", "das_warp_kernel.cuh"]
 

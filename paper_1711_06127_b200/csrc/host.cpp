@@ -73,6 +73,8 @@ struct supra_bf {
   // and the per-entry channel of each mirror variant
   int32_t* d_cta[3] = {nullptr, nullptr, nullptr};
   int32_t* d_ech = nullptr;
+  uint32_t* d_stage_iv = nullptr;  // [E][C] 16-byte chunk range each trace's taps read (supra_bf_stage_raw)
+  int64_t stage_bytes = 0;         // bytes supra_bf_stage_raw moves per frame
   int sym_order = 1;    // 1, 2 or 4 mirror lines that share one delay set
   bool sym_x = false;   // the 2-line tables pair x-mirrors (rows stay whole)
   int num_sms = 148;
@@ -128,7 +130,7 @@ cudaError_t upload(T** d, const std::vector<T>& h) {
 void free_all(supra_bf* h) {
   void* ptrs[] = {h->d_cta[0], h->d_cta[1], h->d_cta[2], h->d_ech,
                   h->d_line_group, h->d_entries, h->d_nentries, h->d_ncount, h->d_line_dir, h->d_line_event,
-                  h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_blk_kmin, h->d_col_l0, h->d_col_nl, h->d_rows, h->d_ent};
+                  h->d_fir, h->d_frame_max, h->d_env, h->d_ax, h->d_az, h->d_blk_kmin, h->d_col_l0, h->d_col_nl, h->d_rows, h->d_ent, h->d_stage_iv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h->mcache.clear();
@@ -569,6 +571,24 @@ supra_status build_das_tables(supra_bf* h) {
   }
   h->info[3] = ref * 2;
   h->info[4] = taps;
+  // staging ranges (supra_bf_stage_raw): per trace the hull of its
+  // referenced samples, widened by one sample each side (the device's float
+  // tau may floor one sample off the binary64 value at an integer) and
+  // rounded out to 16-byte chunks
+  std::vector<uint32_t> siv((size_t)h->E * C, 0u);
+  int64_t sbytes = 0;
+  for (size_t t = 0; t < iv.size(); t++) {
+    if (iv[t].empty()) continue;
+    long lo = iv[t][0].first, hi = iv[t][0].second;
+    for (auto& pr : iv[t]) { lo = std::min(lo, pr.first); hi = std::max(hi, pr.second); }
+    const long c0 = std::max(0L, lo - 1) / 8, c1 = std::min((long)S, hi + 2 + 7) / 8;
+    siv[t] = (uint32_t)c0 | ((uint32_t)c1 << 16);
+    sbytes += (c1 - c0) * 16;
+  }
+  h->stage_bytes = sbytes;
+  if ((e = upload(&h->d_stage_iv, siv)) != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? SUPRA_E_RESOURCE : SUPRA_E_CUDA, "table upload: %s",
+                cudaGetErrorString(e));
   return SUPRA_OK;
 }
 
@@ -956,6 +976,32 @@ supra_status supra_bf_set_das_events(supra_bf_t h, void* before, void* after) {
   h->ev_before = (cudaEvent_t)before;
   h->ev_after = (cudaEvent_t)after;
   return SUPRA_OK;
+}
+
+supra_status supra_bf_stage_raw(supra_bf_t h, const void* src, void* dst, int32_t frames, int64_t* bytes_per_frame,
+                                void* stream) {
+  g_err.clear();
+  if (!h) return fail(SUPRA_E_STRUCT, "handle is NULL");
+  if (bytes_per_frame) *bytes_per_frame = h->stage_bytes;
+  if (frames < 0 || frames > h->cfg.max_frames_per_call)
+    return fail(SUPRA_E_STRUCT, "frames %d outside [0, %d]", frames, h->cfg.max_frames_per_call);
+  if (!src || !dst) return fail(SUPRA_E_STRUCT, "src and dst must not be NULL");
+  if (((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return fail(SUPRA_E_STRUCT, "src / dst must be 16-byte aligned");
+  if (frames == 0) return SUPRA_OK;
+  DeviceGuard dg(h->cfg.device);
+  if (!is_device_ptr(dst, h->cfg.device)) return fail(SUPRA_E_STRUCT, "dst is not device memory of device %d", h->cfg.device);
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, src) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SUPRA_E_STRUCT, "src is neither device nor page-locked host memory");
+  }
+  const bool src_ok = pa.type == cudaMemoryTypeHost || ((pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged) &&
+                                                        pa.device == h->cfg.device);
+  if (!src_ok) return fail(SUPRA_E_STRUCT, "src is neither page-locked host memory nor device memory of device %d",
+                           h->cfg.device);
+  const void* s = pa.type == cudaMemoryTypeHost && pa.devicePointer ? pa.devicePointer : src;
+  return check_launch(launch_stage_raw(s, dst, h->d_stage_iv, h->E * h->C, h->S, frames, (cudaStream_t)stream),
+                      "stage kernel");
 }
 
 supra_status supra_bf_info(supra_bf_t h, int64_t* info8) {

@@ -240,6 +240,9 @@ cudaError_t launch_das_warp(const CUtensorMap& raw_map, const DasArgs& a, cudaSt
 size_t das_smem_bytes(int fb, int nt, int nent_max, int fir_taps, int mir);
 cudaError_t launch_envlog(const EnvArgs& a, cudaStream_t st);
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+// iv[e * C + c] = 16-byte chunk range [lo, hi) of trace (e, c) (lo | hi << 16)
+cudaError_t launch_stage_raw(const void* src, void* dst, const uint32_t* iv, int traces_per_frame, int S,
+                             int frames, cudaStream_t st);
 cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaStream_t st);
 cudaError_t launch_sc_table(const ScArgs& a, int line_img_bytes_per_frame, cudaStream_t st);
 

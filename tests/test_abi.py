@@ -120,6 +120,7 @@ def test_null_handle_calls():
     assert L.supra_bf_beamform(None, None, 1, None, None, None) == binding.E_STRUCT
     assert L.supra_bf_envelope_log(None, None, 1, None, None) == binding.E_STRUCT
     assert L.supra_bf_scanconvert(None, None, 1, None, None, None) == binding.E_STRUCT
+    assert L.supra_bf_stage_raw(None, None, None, 1, None, None) == binding.E_STRUCT
     L.supra_bf_destroy(None)
     assert _create.__name__  # destroy(NULL) is a no-op
 
