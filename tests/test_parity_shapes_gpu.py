@@ -8,14 +8,18 @@ on sampled scanlines -- the oracle costs ~70 ms per C4 line per core -- with
 a FIXED log reference taken from the oracle's envelope, so the fused line
 image of the sampled lines is comparable line by line.
 
-Shapes (das_shape in csrc/das.cu):
-  C2 100 frames        <16,4> + remainder <4,8>    (headline)
-  C4b 8 volumes        <8,4>                       (bench C4b_stream)
-  C4p 4 volumes        <4,16>, S = 3648            (bench C4p_stream)
-  C4a / C4b 1 volume   warp-split, S = 2048        (bench C4a_single, C4b_single)
-  C4p 1 volume         <1,16>                      (bench C4p_single)
+Shapes: whatever pick_shape (csrc/host.cpp) chooses for the bench's call --
+frames per CTA x tiles per pass x mirror lines per CTA:
+  C2 100 frames        <16,4> + remainder launch   (headline)
+  C4b 8 volumes        mirror lines, 8-volume batch (bench C4b_stream)
+  C4p 4 volumes        S = 3648, mirror pairs       (bench C4p_stream)
+  C4a / C4b 1 volume   mirror quads <1,8,MIR=4>     (bench C4a_single, C4b_single)
+  C4p 1 volume         mirror pairs <1,16,MIR=2>    (bench C4p_single)
   T1 64 frames         <16,4>, S = 2368 (3rd pass partial)   (bench T1_*)
-  PSF 1 frame          <1,8>, S = 1408             (tests/test_psf_gpu.py)
+  PSF 1 frame          linear, single frame, S = 1408 (tests/test_psf_gpu.py)
+Every shape sums each output's members in the same fixed order (DESIGN
+reading B6), so results do not depend on the shape; the batch-invariance
+tests below check that bitwise.
 """
 import numpy as np
 import pytest
