@@ -192,21 +192,28 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
       ref = __uint_as_float(a.frame_max[f]);
       lref = ref > 0.f ? lg2_approx(ref) : 0.f;
     }
+    // (rows without a valid k0 read the slab's first samples and select 0:
+    // every read stays inside the slab, the loop has no divergent branch)
+    const bool rowok = lane < rows && az.i0 >= 0;
+    const float* py = slab(b) + wl0 * kstride + (rowok ? az.i0 - (use_tma ? kal : kmin) : 0);
+    float2* pt = tz + lane * TZS;
     float tprev = 0.f;
-    for (int j = 0; j < wnl; j++) {
-      const float* y = slab(b) + (wl0 + j) * kstride - (use_tma ? kal : kmin);
-      float t = 0.f;
-      if (lane < rows && az.i0 >= 0) {
-        float y0 = y[az.i0], y1 = y[az.i0 + 1];
-        if (a.frame_max) {
-          y0 = y_of_env(y0, ref, lref, a.DR_k);
-          y1 = y_of_env(y1, ref, lref, a.DR_k);
-        }
-        t = fmaf(az.f, y1 - y0, y0);
+    if (a.frame_max) {
+      for (int j = 0; j < wnl; j++, py += kstride) {
+        const float y0 = y_of_env(py[0], ref, lref, a.DR_k), y1 = y_of_env(py[1], ref, lref, a.DR_k);
+        float t = rowok ? fmaf(az.f, y1 - y0, y0) : 0.f;
+        if (U8OUT) t = fmaf(255.f, t, 0.5f);
+        if (j > 0 && lane < rows) pt[j - 1] = make_float2(tprev, t - tprev);
+        tprev = t;
       }
-      if (U8OUT) t = fmaf(255.f, t, 0.5f);
-      if (j > 0 && lane < rows) tz[lane * TZS + j - 1] = make_float2(tprev, t - tprev);
-      tprev = t;
+    } else {
+      for (int j = 0; j < wnl; j++, py += kstride) {
+        const float y0 = py[0], y1 = py[1];
+        float t = rowok ? fmaf(az.f, y1 - y0, y0) : 0.f;
+        if (U8OUT) t = fmaf(255.f, t, 0.5f);
+        if (j > 0 && lane < rows) pt[j - 1] = make_float2(tprev, t - tprev);
+        tprev = t;
+      }
     }
     __syncwarp();
     if (use_tma && lane == 0)
