@@ -2,7 +2,9 @@
 racecheck / synccheck): single-frame warp-split DAS (Hann and Hamming, t0,
 nearest), batch DAS with row-cut maps and a PDL remainder launch, band
 bank + decimation, channel map, linear / sector / pyramid scan conversion,
-standalone envelope, line-range split.  Dev/validation aid."""
+standalone envelope, line-range split; mirror-line DAS (pairs on a small
+phased sector, quads on a small matrix probe), the 3D table scan
+conversion and the input staging from pinned host memory.  Dev/validation aid."""
 import os
 import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -42,4 +44,24 @@ run(configs.c3(num_lines_x=16, line_origin_mm=configs.phased_lines(16, 60.0)[0],
                line_direction=configs.phased_lines(16, 60.0)[1], num_events=16,
                line_event=__import__("numpy").arange(16, dtype="int32"),
                tx_origin_mm=__import__("numpy").zeros((16, 3)), S=1024), 2)
+# small 4-fold symmetric matrix probe: mirror quads, pyramid scan conversion
+import numpy as np  # noqa: E402
+o, d = configs.phased_lines(8, 60.0, 8, 60.0)
+ev = np.arange(64, dtype=np.int32)
+S = 512
+sp = (S - 1) * configs.dr_mm() / 31
+wm = configs.Workload("C4s", 8, 8, 0.3, 0.3, 7e6, 64, S, 8, 8, o, d, ev, configs.tx_origins(o, ev, 64),
+                      configs.SC_PYRAMID_3D, (32, 32, 32), (-15.5 * sp, -15.5 * sp, 0.0), (sp, sp, sp),
+                      fov_x_deg=60.0, fov_y_deg=60.0, noise_db=-40.0)
+run(wm, 1)
+run(wm, 3)
+# input staging from pinned host memory
+w = configs.c2()
+bf = SupraBF(w, max_frames=2)
+raw = raw_frames(w, 2)
+dst = torch.empty_like(raw)
+bf.stage_raw(raw.cpu().pin_memory(), dst, 2)
+torch.cuda.synchronize()
+bf.close()
+print("ok stage", flush=True)
 print("all ok")
