@@ -24,8 +24,10 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
       : "memory");
 }
 
-// try_wait with a suspend-time hint: the warp sleeps in hardware until the
-// phase completes (or ~the hint elapses) instead of spinning on issue slots.
+// mbarrier.try_wait blocks for a hardware-defined window, then the loop
+// retries.  (Measured: a suspend-time hint, or __nanosleep back-off of
+// 32-500 ns between tries, is no faster -- the retries' issue slots are not
+// what bounds the DAS kernels.)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
