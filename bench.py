@@ -570,8 +570,9 @@ def secondary_all(dev_index: int, world: int, rank: int):
                                        "hbm", ctx3d)
     out["C4p_stream"] = secondary_line("C4p", configs.c4p(**u8), 4, 5, dev_index, world, "volumes/s",
                                        "hbm", ctx3d)
-    # BASELINE configs[2]: phased 128 el, 192 lines, 4096 samples, sector 512^2
-    out["C3"] = secondary_line("C3", configs.c3(sc_output_type=configs.T_U8), 16, 10, dev_index, world,
+    # BASELINE configs[2]: phased 128 el, 192 lines, 4096 samples, sector 512^2;
+    # 32 frames per call (SURVEY 8(d) protocol: 2D >= 25 frames per call)
+    out["C3"] = secondary_line("C3", configs.c3(sc_output_type=configs.T_U8), 32, 10, dev_index, world,
                                "frames/s", "hbm")
     for name, fps in PAPER_T1_GTX1080_FPS.items():
         out[name] = secondary_line(name, configs.CONFIGS[name](**u8), 64, 10, dev_index, world, "frames/s",

@@ -501,18 +501,18 @@ def test_beamform_bmode_equals_two_calls(name, F, over):
 
 
 def test_c3_bench_launch_configuration():
-    """C3 as the bench times it: 16 frames per call (FB = 16, four 1024-sample
-    depth passes with carried FIR halos, row-cut windows), u8 sector B-mode;
-    frames 0 and 15 vs the oracle chain."""
+    """C3 as the bench times it: 32 frames per call (16 virtual frames per
+    CTA, four 1024-sample depth passes with carried FIR halos, row-cut
+    windows), u8 sector B-mode; frames 0 and 31 vs the oracle chain."""
     w = configs.c3(sc_output_type=configs.T_U8)
-    F = 16
+    F = 32
     raw = raw_frames(w, F)
     bf = SupraBF(w, max_frames=F)
     rf_g, y_g = run_gpu(bf, raw, F)
     img = bf.empty_img(F)
     bf.scanconvert(torch.from_numpy(y_g).cuda(), F, img)
     torch.cuda.synchronize()
-    for f in (0, 15):
+    for f in (0, F - 1):
         e_rf, e_db, _, env_o = check_frame(w, raw[f].cpu().numpy(), rf_g[f], y_g[f])
         assert e_rf <= RF_TOL and e_db <= DB_TOL, (f, e_rf, e_db)
         y_o, _ = oracle.log_compress(env_o, 50.0)
