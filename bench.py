@@ -562,11 +562,16 @@ def secondary_all(dev_index: int, world: int, rank: int):
     out["C4a_single"] = secondary_line("C4a", configs.c4("a", **u8), 1, 5, dev_index, world, "volumes/s",
                                        "hbm", {"lines": 4096, "events": 4096,
                                                "note": "M = 1: 16 GiB of int16 per volume, HBM-bound"})
+    # the same volumes streamed two per call (32 GiB of input per call): the
+    # mirror-quad CTAs take both volumes, sharing each tap's geometry by 8
+    out["C4a_stream"] = secondary_line("C4a_stream", configs.c4("a", **u8), 2, 5, dev_index, world, "volumes/s",
+                                       "hbm", {"lines": 4096, "events": 4096,
+                                               "note": "M = 1, 2 volumes per call: HBM-bound"})
     out["C4b_stream"] = secondary_line("C4b", configs.c4("b", **u8), 8, 5, dev_index, world, "volumes/s",
                                        "alu", {"note": "4x4 multi-line (each sample feeds 16 lines): ALU-bound"})
     out["C4b_single"] = secondary_c4b_single(dev_index, world, rank)
     # the paper's 3D row: 384 channels, 32x16 lines, 70 mm, 401x401x402
-    out["C4p_single"] = secondary_line("C4p", configs.c4p(**u8), 1, 10, dev_index, world, "volumes/s",
+    out["C4p_single"] = secondary_line("C4p_1", configs.c4p(**u8), 1, 10, dev_index, world, "volumes/s",
                                        "hbm", ctx3d)
     out["C4p_stream"] = secondary_line("C4p", configs.c4p(**u8), 4, 5, dev_index, world, "volumes/s",
                                        "hbm", ctx3d)

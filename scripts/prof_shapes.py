@@ -22,7 +22,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # key -> (config, frames per call, DAS launches per call)
 SHAPES = {
-    "C2": ("C2", 100, 2), "C3": ("C3", 32, 1), "C4a": ("C4a", 1, 1), "C4b": ("C4b", 8, 1),
+    "C2": ("C2", 100, 2), "C3": ("C3", 32, 1), "C4a": ("C4a", 1, 1), "C4a_stream": ("C4a", 2, 1), "C4b": ("C4b", 8, 1),
     "C4b_1": ("C4b", 1, 1), "C4p": ("C4p", 4, 1), "C4p_1": ("C4p", 1, 1),
     "T1_64_1": ("T1_64_1", 64, 1), "T1_64_2": ("T1_64_2", 64, 1),
     "T1_128_1": ("T1_128_1", 64, 1), "T1_128_2": ("T1_128_2", 64, 1),

@@ -90,9 +90,29 @@ def test_c4b_stream_shape_8_volumes():
     sampled_fixed_ref_parity(w, raw, 8, c4_lines(w, 21), check_vols=(0, 5, 7))
 
 
+def test_c4a_stream_shape_2_volumes_and_batch_invariance():
+    # bench C4a_stream: two 16 GiB volumes per call (mirror quads, 2 volumes
+    # per CTA); the oracle on sampled lines of both, and each volume's RF and
+    # line image bitwise equal to its own single-volume call (reading B6)
+    w = configs.c4("a")
+    raw = distinct_volumes(w, 2)
+    sampled_fixed_ref_parity(w, raw, 2, c4_lines(w, 25, n=6), check_vols=(0, 1))
+    bf = SupraBF(w, max_frames=2)
+    rf2, li2 = bf.empty_rf(2), bf.empty_line_img(2)
+    bf.beamform(raw, 2, rf=rf2, line_img=li2)
+    for v in range(2):
+        rf1, li1 = bf.empty_rf(1), bf.empty_line_img(1)
+        bf.beamform(raw[v:v + 1], 1, rf=rf1, line_img=li1)
+        torch.cuda.synchronize()
+        assert torch.equal(rf1[0], rf2[v]), v
+        assert torch.equal(li1[0], li2[v]), v
+        del rf1, li1
+    bf.close()
+
+
 @pytest.mark.parametrize("variant", ["a", "b"])
 def test_c4_single_volume_fused_line_image(variant):
-    # the warp-split single-volume kernel with its fused envelope/log epilogue
+    # one volume per call (mirror quads) with the fused envelope/log epilogue
     w = configs.c4(variant)
     raw = distinct_volumes(w, 1)
     sampled_fixed_ref_parity(w, raw, 1, c4_lines(w, 22), check_vols=(0,))
