@@ -1321,24 +1321,29 @@ static supra_status run_sc(supra_bf_t h, const void* line_img, int in_type, cons
   a.rows = h->d_rows;
   a.ent = h->d_ent;
   a.is3d = c.sc_kind == SUPRA_SC_PYRAMID_3D;
-  // bulk-copy staging of the slab: 16-byte aligned line segments
-  a.slab_tma = (c.sc_kind == SUPRA_SC_LINEAR_2D && h->sc_tiled && in_type == SUPRA_T_F32 &&
-                (h->Sd % 4) == 0 && ((uintptr_t)line_img & 15) == 0)
-                   ? 1
-                   : 0;
-  // one 2-D tensor map over the [frames Lx][Sd] f32 line image: a single
-  // TMA per (tile, frame) instead of one bulk copy per line (1-D fallback if
-  // the encode fails)
+  // bulk-copy staging of the slab: 16-byte aligned line segments (f32; a
+  // u8 line image needs the tensor copy below, else the kernel's own loads)
+  const bool in8 = in_type == SUPRA_T_U8;
+  const int esz = in8 ? 1 : 4;
+  const bool slab_ok = c.sc_kind == SUPRA_SC_LINEAR_2D && h->sc_tiled && (h->Sd * esz) % 16 == 0 &&
+                       ((uintptr_t)line_img & 15) == 0;
+  a.slab_tma = (slab_ok && !in8) ? 1 : 0;
+  // u8: segments start 16-byte aligned (k & ~15), box width a multiple of 16
+  if (in8) a.slab_box_k = std::min(256, (h->slab_k + 15 + 15) & ~15);
+  // one 2-D tensor map over the [frames Lx][Sd] line image: a single TMA per
+  // (tile, frame) instead of one bulk copy per line (fallback if the encode
+  // fails)
   CUtensorMap slab_map;
   const CUtensorMap* sm = nullptr;
-  if (a.slab_tma && frames > 0) {
+  if (slab_ok && frames > 0) {
     EncodeTiledFn fn = encode_fn();
     cuuint64_t dims[2] = {(cuuint64_t)h->Sd, (cuuint64_t)frames * c.num_lines_x};
-    cuuint64_t strides[1] = {(cuuint64_t)h->Sd * 4};
-    cuuint32_t box[2] = {(cuuint32_t)h->sc_box_k, (cuuint32_t)h->sc_box_l};
+    cuuint64_t strides[1] = {(cuuint64_t)h->Sd * esz};
+    cuuint32_t box[2] = {(cuuint32_t)a.slab_box_k, (cuuint32_t)h->sc_box_l};
     cuuint32_t es[2] = {1, 1};
-    if (fn && fn(&slab_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(line_img), dims, strides, box,
-                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    if (fn && fn(&slab_map, in8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                 const_cast<void*>(line_img), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
       sm = &slab_map;
       a.slab_tma = 2;

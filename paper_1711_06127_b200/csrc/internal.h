@@ -193,8 +193,8 @@ struct ScArgs {
   const int32_t* col_l0;    // [ceil(nx / 256)]: first line the column tile touches
   const int32_t* col_nl;    // [ceil(nx / 256)]: lines it touches (0: none valid)
   int tiled;             // 1: tiled separable kernel; 0: direct per-pixel kernel
-  int slab_tma;          // 1: stage the slab with 1-D bulk copies, 2: one 2-D tensor copy (f32 line image)
-  int slab_box_k, slab_box_l;  // staged segment: samples (multiple of 4) x lines
+  int slab_tma;          // 1: stage the slab with 1-D bulk copies (f32), 2: one 2-D tensor copy (f32 or u8 line image)
+  int slab_box_k, slab_box_l;  // staged segment: samples (16 bytes multiple) x lines
   // table
   const ScRow* rows;     // [nz*ny]
   const ScEntry* ent;

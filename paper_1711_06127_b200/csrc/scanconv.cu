@@ -57,15 +57,23 @@ __device__ __forceinline__ void store_img(void* p, int type, size_t i, float v) 
 // row) into its own small buffer, so the two phases need only __syncwarp;
 // a per-buffer "empty" mbarrier (8 warp arrivals) gates the refill.
 constexpr int kScWarpLines = kScWarpLinesMax + 1;  // + the zero pair
-template <bool U8OUT>
+// Slab elements of one buffer (as sized by launch_sc_linear): a multiple of
+// 128 bytes, so both buffers are 128-byte aligned TMA destinations.
+__host__ __device__ inline int sc_slab_elems(int box_l, int box_k, int slab_k, int elem_bytes) {
+  const int q = 128 / elem_bytes;
+  return (box_l * (box_k > slab_k ? box_k : slab_k) + q - 1) / q * q;
+}
+// IN8: u8 line image (log-compressed, y = v / 255), staged as bytes -- a
+// quarter of the f32 slab -- by the same 2-D tensor copy.
+template <bool U8OUT, bool IN8>
 __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_constant__ CUtensorMap tm,
                                                               const ScArgs a, int fpc) {
+  using T = typename std::conditional<IN8, uint8_t, float>::type;
   // the two slab buffers live in dynamic shared memory (the pair buffers
   // below are static; together they exceed the 48 KB static limit)
-  extern __shared__ __align__(128) float slab_dyn[];
-  // per buffer (as sized by launch_sc_linear); 128-byte aligned TMA destinations
-  const int slab_elems = (a.slab_box_l * max(a.slab_box_k, a.slab_k) + 31) & ~31;
-  auto slab = [&](int b) { return slab_dyn + b * slab_elems; };
+  extern __shared__ __align__(128) unsigned char slab_raw[];
+  const int slab_elems = sc_slab_elems(a.slab_box_l, a.slab_box_k, a.slab_k, (int)sizeof(T));
+  auto slab = [&](int b) { return reinterpret_cast<T*>(slab_raw) + b * slab_elems; };
   // per warp and output row: pairs {t(j), t(j+1) - t(j)} of the depth-lerped
   // lines (u8: t scaled to 255 t + 1/2), so a pixel is one LDS.64 + FFMA;
   // odd row stride in 8-byte units: conflict-free 64-bit row writes
@@ -83,9 +91,9 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
   const int Lx = a.Lx, S = a.S, nx = a.nx;
   const int rows = min(kScRows, a.nz - z0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool use_tma = a.in_type == SUPRA_T_F32 && a.slab_tma;
+  const bool use_tma = a.slab_tma != 0;
   const int kstride = use_tma ? a.slab_box_k : ks;    // slab row stride (samples)
-  const int kal = kmin & ~3;                           // 16-byte aligned segment start
+  const int kal = kmin & (IN8 ? ~15 : ~3);             // 16-byte aligned segment start
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; b++) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[b])),
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
     if (a.slab_tma == 2) {
       const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&full[b]);
       const unsigned bytes =
-          (lane == 0 && kmin >= 0 && nl > 0) ? (unsigned)(a.slab_box_k * a.slab_box_l) * 4u : 0u;
+          (lane == 0 && kmin >= 0 && nl > 0) ? (unsigned)(a.slab_box_k * a.slab_box_l * (int)sizeof(T)) : 0u;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
       if (bytes)
@@ -139,6 +147,7 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
             : "memory");
       return;
     }
+    // (1-D bulk copies: f32 line images only, see run_sc)
     const float* src = (const float*)a.line_img + (size_t)f * Lx * S;
     const int seg = min(a.slab_box_k, S - kal);
     const uint32_t bb = (uint32_t)__cvta_generic_to_shared(&full[b]);
@@ -149,7 +158,7 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
     for (int l = lane; l < nl && kmin >= 0; l += 32)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              (uint32_t)__cvta_generic_to_shared(slab(b) + l * a.slab_box_k)),
+              (uint32_t)__cvta_generic_to_shared(reinterpret_cast<float*>(slab(b)) + l * a.slab_box_k)),
           "l"(src + (size_t)(l0 + l) * S + kal), "r"((unsigned)seg * 4u), "r"(bb)
           : "memory");
   };
@@ -169,17 +178,16 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
       if (it > 0) __syncthreads();  // every warp is done with slab(0)
       if (kmin >= 0 && nl > 0) {
         const size_t fbase = (size_t)f * Lx * S;
-        if (a.in_type == SUPRA_T_F32) {
+        if constexpr (!IN8) {
           const float* src = (const float*)a.line_img + fbase;
           for (int l = warp; l < nl; l += 8)
             for (int kk = lane; kk < ks; kk += 32)
               cp_async4(slab(0) + l * ks + kk, src + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
           asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
         } else {
+          const uint8_t* src = (const uint8_t*)a.line_img + fbase;
           for (int l = warp; l < nl; l += 8)
-            for (int kk = lane; kk < ks; kk += 32)
-              slab(0)[l * ks + kk] =
-                  load_y(a.line_img, a.in_type, fbase + (size_t)(l0 + l) * S + min(kmin + kk, S - 1));
+            for (int kk = lane; kk < ks; kk += 32) slab(0)[l * ks + kk] = src[(size_t)(l0 + l) * S + min(kmin + kk, S - 1)];
         }
       }
       __syncthreads();
@@ -195,12 +203,15 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
     // (rows without a valid k0 read the slab's first samples and select 0:
     // every read stays inside the slab, the loop has no divergent branch)
     const bool rowok = lane < rows && az.i0 >= 0;
-    const float* py = slab(b) + wl0 * kstride + (rowok ? az.i0 - (use_tma ? kal : kmin) : 0);
+    const T* py = slab(b) + wl0 * kstride + (rowok ? az.i0 - (use_tma ? kal : kmin) : 0);
     float2* pt = tz + lane * TZS;
     float tprev = 0.f;
-    if (a.frame_max) {
+    // u8 samples: y = fl(v fl(1/255)) (load_y's expression), rounded on its
+    // own (no contraction into the lerp), as if staged from an f32 image
+    auto yv = [](T v) { return IN8 ? __fmul_rn((float)v, 1.0f / 255.0f) : (float)v; };
+    if (!IN8 && a.frame_max) {
       for (int j = 0; j < wnl; j++, py += kstride) {
-        const float y0 = y_of_env(py[0], ref, lref, a.DR_k), y1 = y_of_env(py[1], ref, lref, a.DR_k);
+        const float y0 = y_of_env(yv(py[0]), ref, lref, a.DR_k), y1 = y_of_env(yv(py[1]), ref, lref, a.DR_k);
         float t = rowok ? fmaf(az.f, y1 - y0, y0) : 0.f;
         if (U8OUT) t = fmaf(255.f, t, 0.5f);
         if (j > 0 && lane < rows) pt[j - 1] = make_float2(tprev, t - tprev);
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(256) sc_linear_tiled_kernel(const __grid_const
       }
     } else {
       for (int j = 0; j < wnl; j++, py += kstride) {
-        const float y0 = py[0], y1 = py[1];
+        const float y0 = yv(py[0]), y1 = yv(py[1]);
         float t = rowok ? fmaf(az.f, y1 - y0, y0) : 0.f;
         if (U8OUT) t = fmaf(255.f, t, 0.5f);
         if (j > 0 && lane < rows) pt[j - 1] = make_float2(tprev, t - tprev);
@@ -396,14 +407,15 @@ cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaS
   dim3 grid((a.nx + 255) / 256, (a.nz + kScRows - 1) / kScRows, (a.F + fpc - 1) / fpc);
   CUtensorMap none{};
   const CUtensorMap& tm = slab_map ? *slab_map : none;
-  const size_t smem = 2 * (size_t)((a.slab_box_l * std::max(a.slab_box_k, a.slab_k) + 31) & ~31) * sizeof(float);
-  if (a.out_type == SUPRA_T_U8) {
-    cudaFuncSetAttribute(sc_linear_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sc_linear_tiled_kernel<true><<<grid, 256, smem, st>>>(tm, a, fpc);
-  } else {
-    cudaFuncSetAttribute(sc_linear_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sc_linear_tiled_kernel<false><<<grid, 256, smem, st>>>(tm, a, fpc);
-  }
+  const bool in8 = a.in_type == SUPRA_T_U8;
+  const size_t smem =
+      2 * (size_t)sc_slab_elems(a.slab_box_l, a.slab_box_k, a.slab_k, in8 ? 1 : 4) * (in8 ? 1 : 4);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, st>>>(tm, a, fpc);
+  };
+  if (a.out_type == SUPRA_T_U8) in8 ? go(sc_linear_tiled_kernel<true, true>) : go(sc_linear_tiled_kernel<true, false>);
+  else in8 ? go(sc_linear_tiled_kernel<false, true>) : go(sc_linear_tiled_kernel<false, false>);
   return cudaGetLastError();
 }
 

@@ -259,3 +259,42 @@ def test_sector_decimation_sc_indices():
     v = valid_o.astype(bool)
     assert np.array_equal(idx_g[v], idx_o[v])
     assert idx_g[v][:, 2].max() < w.S // 2
+
+
+# ----------------- linear scan conversion from a u8 line image (the bench's
+# Table-1 lines): the 2-D tensor copy stages the bytes (a quarter of the f32
+# slab), the depth lerp reads y = v / 255.
+@pytest.mark.parametrize("name,F", [("C2", 3), ("T1_64_1", 5)])
+def test_linear_sc_u8_line_image(name, F):
+    w8 = configs.CONFIGS[name]().replace(line_output_type=configs.T_U8, sc_output_type=configs.T_F32)
+    g = torch.Generator().manual_seed(7)
+    L, S = w8.L, w8.S
+    li8 = torch.randint(0, 256, (F, L, S), generator=g, dtype=torch.uint8)
+    bf8 = SupraBF(w8, max_frames=F)
+    img = bf8.empty_img(F)
+    mask = bf8.empty_mask()
+    bf8.scanconvert(li8.cuda(), F, img, mask)
+    # the same values as an f32 line image (v * fl(1/255) in f32, the
+    # kernel's own conversion): the f32 path must give the same bits
+    wf = w8.replace(line_output_type=configs.T_F32)
+    bff = SupraBF(wf, max_frames=F)
+    lif = (li8.to(torch.float32) * torch.tensor(1.0 / 255.0, dtype=torch.float32)).cuda()
+    imgf = bff.empty_img(F)
+    bff.scanconvert(lif, F, imgf)
+    torch.cuda.synchronize()
+    assert torch.equal(img, imgf)
+    # vs the oracle (binary64) on the first and last frame
+    for f in (0, F - 1):
+        img_o, mask_o = oracle.scan_convert(w8, li8[f].numpy().astype(np.float64) / 255.0)
+        assert np.array_equal(mask.cpu().numpy().reshape(mask_o.shape), mask_o)
+        assert db_err(img.cpu().numpy()[f].reshape(img_o.shape), img_o) <= DB_TOL
+    # u8 B-mode from the u8 line image: within one LSB of the oracle
+    wu = w8.replace(sc_output_type=configs.T_U8)
+    bfu = SupraBF(wu, max_frames=F)
+    imgu = bfu.empty_img(F)
+    bfu.scanconvert(li8.cuda(), F, imgu)
+    img_o, _ = oracle.scan_convert(wu, li8[F - 1].numpy().astype(np.float64) / 255.0)
+    d = imgu.cpu().numpy()[F - 1].reshape(img_o.shape).astype(int) - oracle.to_u8(img_o).astype(int)
+    assert np.max(np.abs(d)) <= 1
+    for b in (bf8, bff, bfu):
+        b.close()
