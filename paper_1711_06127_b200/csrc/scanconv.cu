@@ -314,14 +314,42 @@ __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(
 // (double-buffered, persistent CTAs) or z-major warp tiles (4 x by 8 z per
 // warp, ~5 L1 lines per gather instead of ~15) were both slower
 // (60 vs 52 us per C4 volume).
+// Rows are walked by each warp with a stride of the grid's warp count; the
+// next row's record is loaded and its entry span bulk-prefetched into L2
+// while the current row is blended (the entry loads were the DRAM-latency
+// stall: long-scoreboard on the first use of each entry, ~18 % of samples).
+__device__ __forceinline__ void l2_prefetch_span(const void* p, uint32_t bytes) {
+  const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
+  const uint32_t n = (uint32_t)((((uintptr_t)p + bytes + 15) & ~(uintptr_t)15) - a0);
+  if (n)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
+}
+
 template <int IN_T, int OUT_T, bool IS3D, bool LOGLOAD>
 __global__ void __launch_bounds__(256, 4) sc_table_kernel(const ScArgs a, int fpc) {
   constexpr int V = 4;  // voxels per lane and chunk
   const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (r >= a.nz * a.ny) return;
+  const int nrows = a.nz * a.ny;
+  const int rstride = gridDim.x * 8;
+  int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= nrows) return;
   const int f0 = blockIdx.y * fpc, f1 = min(a.F, f0 + fpc);
-  const ScRow row = a.rows[r];
+  auto prefetch_row = [&](const ScRow& q) {
+    if (lane == 0 && q.xhi > q.xlo)
+      l2_prefetch_span(reinterpret_cast<const uint2*>(a.ent) + q.off, (uint32_t)(q.xhi - q.xlo) * 8u);
+  };
+  ScRow nrow = a.rows[r];
+  prefetch_row(nrow);
+  ScRow nnrow = r + rstride < nrows ? a.rows[r + rstride] : nrow;
+  for (; r < nrows; r += rstride) {
+  const ScRow row = nrow;
+  if (r + rstride < nrows) {
+    // next row: its entries into L2 now; the record after it loads while
+    // this row is blended
+    nrow = nnrow;
+    prefetch_row(nrow);
+    if (r + 2 * rstride < nrows) nnrow = a.rows[r + 2 * rstride];
+  }
   const uint32_t S = (uint32_t)a.S, LS = (uint32_t)a.Lx * S;
   const size_t fstride = (size_t)a.Ly * LS;  // line-image elements per frame
   const size_t ostride = (size_t)a.nz * a.ny * a.nx;
@@ -331,7 +359,28 @@ __global__ void __launch_bounds__(256, 4) sc_table_kernel(const ScArgs a, int fp
   // by 1/255 once at the end
   constexpr float kInScale = IN_T == SUPRA_T_U8 ? 1.0f / 255.0f : 1.0f;
   const uint2* rent = reinterpret_cast<const uint2*>(a.ent) + row.off - row.xlo;  // entry of column x: rent[x]
-  for (int x0 = 0; x0 < a.nx; x0 += 32 * V) {
+  // columns outside the row's valid range [xlo, xhi): zeros (and mask 0)
+  {
+    const int xlo = max(0, min(row.xlo, a.nx)), xhi = max(xlo, min(row.xhi, a.nx));
+    for (int f = f0; f < f1; f++) {
+      const size_t ob = (size_t)f * ostride + (size_t)r * a.nx;
+      for (int x = lane; x < xlo; x += 32) {
+        if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = 0;
+        else ((float*)a.img)[ob + x] = 0.f;
+      }
+      for (int x = xhi + lane; x < a.nx; x += 32) {
+        if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = 0;
+        else ((float*)a.img)[ob + x] = 0.f;
+      }
+    }
+    if (a.mask && f0 == 0) {
+      for (int x = lane; x < xlo; x += 32) a.mask[(size_t)r * a.nx + x] = 0;
+      for (int x = xhi + lane; x < a.nx; x += 32) a.mask[(size_t)r * a.nx + x] = 0;
+    }
+  }
+  // the valid range, in chunks of 32 V columns
+  const int xend = min(row.xhi, a.nx);
+  for (int x0 = max(0, row.xlo); x0 < xend; x0 += 32 * V) {
     uint32_t base[V];
     float fx[V], fz[V];
 #pragma unroll
@@ -346,7 +395,7 @@ __global__ void __launch_bounds__(256, 4) sc_table_kernel(const ScArgs a, int fp
       }
       fx[j] = u2f(q & 0xFFFFu) * (1.0f / 65535.0f);
       fz[j] = u2f(q >> 16) * (1.0f / 65535.0f);
-      if (a.mask && f0 == 0 && x < a.nx) a.mask[(size_t)r * a.nx + x] = base[j] != kScInvalid ? 1 : 0;
+      if (a.mask && f0 == 0 && x < xend) a.mask[(size_t)r * a.nx + x] = base[j] != kScInvalid ? 1 : 0;
     }
     for (int f = f0; f < f1; f++) {
       float ref = 0.f, lref = 0.f;
@@ -382,13 +431,17 @@ __global__ void __launch_bounds__(256, 4) sc_table_kernel(const ScArgs a, int fp
           }
           v *= kInScale;
         }
-        if (x < a.nx) {
-          if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = (uint8_t)__float2uint_rd(fmaf(255.f, v, 0.5f));
+        if (x < xend) {
+          // u8 = floor(255 v + 1/2) by the magic-number floor (FADD.RM; the
+          // F2I conversion runs at quarter rate)
+          if constexpr (OUT_T == SUPRA_T_U8)
+            ((uint8_t*)a.img)[ob + x] = (uint8_t)__float_as_uint(__fadd_rd(fmaf(255.f, v, 0.5f), 12582912.0f));
           else ((float*)a.img)[ob + x] = v;
         }
       }
     }
   }
+  }  // rows
 }
 
 cudaError_t launch_sc_linear(const ScArgs& a, const CUtensorMap* slab_map, cudaStream_t st) {
@@ -428,7 +481,10 @@ static cudaError_t launch_tab(const ScArgs& a, int line_img_bytes_per_frame, cud
   const long cap = std::max<long>(1, (48L << 20) / std::max(1, line_img_bytes_per_frame));
   const long fill = std::max<long>(1, tiles * a.F / (148L * 4 * 2));
   const int fpc = (int)std::min<long>({(long)a.F, cap, fill, 16L});
-  dim3 grid((unsigned)tiles, (a.F + fpc - 1) / fpc);
+  // each warp walks ~4 rows (the next row's entries prefetched into L2
+  // while the current one is blended), at least 2 waves of 4 CTAs per SM
+  const long ctas = std::min<long>(tiles, std::max<long>(148L * 4 * 2, (tiles + 3) / 4));
+  dim3 grid((unsigned)ctas, (a.F + fpc - 1) / fpc);
   sc_table_kernel<IN_T, OUT_T, IS3D, LG><<<grid, 256, 0, st>>>(a, fpc);
   return cudaGetLastError();
 }
