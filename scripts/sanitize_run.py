@@ -4,7 +4,8 @@ nearest), batch DAS with row-cut maps and a PDL remainder launch, band
 bank + decimation, channel map, linear / sector / pyramid scan conversion,
 standalone envelope, line-range split; mirror-line DAS (pairs on a small
 phased sector, quads on a small matrix probe), the 3D table scan
-conversion and the input staging from pinned host memory.  Dev/validation aid."""
+conversion (f32 and u8 line images) and the input staging from pinned host
+memory.  Dev/validation aid."""
 import os
 import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -55,6 +56,10 @@ wm = configs.Workload("C4s", 8, 8, 0.3, 0.3, 7e6, 64, S, 8, 8, o, d, ev, configs
                       fov_x_deg=60.0, fov_y_deg=60.0, noise_db=-40.0)
 run(wm, 1)
 run(wm, 3)
+# u8 line images: the linear scan conversion's byte slab (2-D tensor copy)
+# and the table scan conversion from u8
+run(configs.table1(64, 1, line_output_type=configs.T_U8, sc_output_type=configs.T_U8), 2)
+run(wm.replace(line_output_type=configs.T_U8, sc_output_type=configs.T_U8), 2)
 # input staging from pinned host memory
 w = configs.c2()
 bf = SupraBF(w, max_frames=2)
