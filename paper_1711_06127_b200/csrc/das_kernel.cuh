@@ -179,7 +179,9 @@ __device__ __forceinline__ TapGeo tile_geo(int m, const DasArgs& a, const float4
   const bool mem = !(m < M0 + tile_gran(NT)) || k >= kenter;
   const float kf = __fadd_rn(kt0f, (float)(m * kTileK));
   const float h = __fmul_rn(0.5f, kf);
-  const float h2 = (m == 0 && k == 0) ? 1e-20f : __fmul_rn(h, h);  // r2 > 0 even at k = 0, q = 0
+  // h^2 + 1e-20: r2 > 0 even at k = 0, q = 0; for k >= 1 (h^2 >= 1/4) the
+  // sum rounds to h^2 exactly, and k = 0 may sit in any tile (pass shift)
+  const float h2 = __fmaf_rn(h, h, 1e-20f);
   float delta = split_delay(r.x, r.y, h, h2);
   if (T0) delta = __fadd_rn(delta, a.t0fs);
   const float tf = __fadd_rd(delta, kFloorMagic);
@@ -207,8 +209,7 @@ __device__ __forceinline__ void tile_geo2(int m, const DasArgs& a, const float4&
   const bool mem1 = !(m + 1 < M0 + tile_gran(NT)) || ka + kTileK >= kenter;
   const float2 kf = make_float2(kt0f + (float)(m * kTileK), kt0f + (float)((m + 1) * kTileK));
   const float2 h = __fmul2_rn(kf, make_float2(0.5f, 0.5f));
-  float2 h2 = __fmul2_rn(h, h);
-  if (m == 0 && ka == 0) h2.x = 1e-20f;
+  const float2 h2 = __ffma2_rn(h, h, make_float2(1e-20f, 1e-20f));  // (tile_geo)
   float2 delta = split_delay2(r.x, r.y, h, h2);
   if (T0) delta = __fadd2_rn(delta, make_float2(a.t0fs, a.t0fs));
   const float2 tf = add_rm2(delta, make_float2(kFloorMagic, kFloorMagic));
@@ -344,7 +345,16 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
         atomicMax(&sm.smax[(4 * curg + q) % FB], __float_as_uint(bmax[q]));
   };
 
-  for (int k0 = 0; k0 < S; k0 += PL) {
+  // Passes end at S: the first starts at kfirst = S - ceil(S / PL) PL <= 0,
+  // so a record that is not a multiple of PL loses its remainder in the
+  // first pass, where the tiles of negative k -- below every k_enter -- are
+  // skipped by the member-tile dispatch, instead of computing the last
+  // pass's tiles past S (Table 1, S = 2368: 12 -> ~9.3 tiles per line and
+  // entry; C4p, S = 3648 in one 4096-sample pass: 16 -> ~15.3).  Member
+  // order per output is that of the global entry sequence whatever the
+  // pass boundaries, so the results do not change.
+  const int kfirst = S - ((S + PL - 1) / PL) * PL;
+  for (int k0 = kfirst; k0 < S; k0 += PL) {
     const int kend = min(S, k0 + PL);
     // entries with a member sample in the pass: the k_enter-sorted prefix
     // with k_enter < kend
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
     for (int m = 0; m < NT; m++) {
       const int k = k0 + m * kTileK + kt;
       float v[VF];
-      if (k < S) {
+      if (k >= 0 && k < S) {
         const int n = (int)ncount[k];
         const float inv = (a.normalize == SUPRA_NORM_NONE) ? 1.f : (n > 0 ? 1.f / (float)n : 0.f);
         if constexpr (VF == 1) {
@@ -490,7 +500,7 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
         }
       } else {
 #pragma unroll
-        for (int b = 0; b < VF; b++) v[b] = 0.f;  // zero padding past the record
+        for (int b = 0; b < VF; b++) v[b] = 0.f;  // zero padding before 0 and past the record
       }
       if (a.do_epilogue) {
         const int pk = fir_pad(k - kbase);
@@ -512,16 +522,17 @@ __global__ void __launch_bounds__(256, das_ctas_per_sm(FB * MIR, NT)) das_fused_
       const int q4 = i / (2 * P + tail), r = i - q4 * (2 * P + tail);
       if (r < 2 * P)
         sm.line[(size_t)q4 * span + fir_pad(r)] =
-            k0 == 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : sm.carry[q4 * 2 * P + r];
+            k0 == kfirst ? make_float4(0.f, 0.f, 0.f, 0.f) : sm.carry[q4 * 2 * P + r];
       else
         sm.line[(size_t)q4 * span + fir_pad(PL + r)] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
     // ---- epilogue: outputs whose taps are complete in this pass ----
-    const int o_begin = k0 == 0 ? 0 : k0 - P;
+    const int o_begin = k0 == kfirst ? 0 : k0 - P;
     const int o_end = kend == S ? S : k0 + PL - P;
-    const int nblk = (o_end - o_begin + 3) / 4;
-    // (o_begin - kbase = P or 2P: a multiple of 4 for the 65-tap default)
+    const int nblk = o_end > o_begin ? (o_end - o_begin + 3) / 4 : 0;
+    // (o_begin - kbase = 2P - kfirst or P: a multiple of 4 for the 65-tap
+    // default, S and PL being multiples of 32)
     const bool p32 = P == 32;
     for (int it = threadIdx.x; it < ng * nblk; it += blockDim.x) {
       const int q4 = it / nblk, blk = it - q4 * nblk;
