@@ -298,3 +298,29 @@ def test_linear_sc_u8_line_image(name, F):
     assert np.max(np.abs(d)) <= 1
     for b in (bf8, bff, bfu):
         b.close()
+
+
+# -------- records that are not a multiple of the pass length: the first pass
+# starts at S - ceil(S/PL) PL < 0 and holds the remainder,
+# down to a single 32-sample row of real samples (S = 1056 with 1024-sample
+# passes); results vs the oracle and bitwise across launch shapes.
+@pytest.mark.parametrize("S", [1056, 1312, 2080])
+def test_short_first_pass(S):
+    w = configs.c1(S=S)
+    raw = torch.empty((16, w.num_events, w.C, w.S), dtype=torch.int16, device="cuda")
+    for f in range(16):
+        synth.channel_data_gpu(w, raw[f], realisation=f % 4)
+    torch.cuda.synchronize()
+    bf = SupraBF(w, max_frames=16)
+    rf16, y16 = run_gpu(bf, raw, 16)
+    rf6, y6 = run_gpu(bf, raw, 6)
+    rf1, y1 = run_gpu(bf, raw, 1)
+    assert np.array_equal(rf16[:6], rf6) and np.array_equal(y16[:6], y6)
+    for f in (0, 5):
+        rf_o, env_o = oracle_chain(w, raw[f].cpu().numpy())
+        assert rf_err(rf16[f], rf_o) <= RF_TOL
+        y_o, _ = oracle.log_compress(env_o, w.dynamic_range_db, w.reference_mode, w.reference_value)
+        assert db_err(y16[f], y_o) <= DB_TOL
+    rf_o, env_o = oracle_chain(w, raw[0].cpu().numpy())
+    assert rf_err(rf1[0], rf_o) <= RF_TOL
+    bf.close()
