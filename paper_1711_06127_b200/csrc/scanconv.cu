@@ -286,13 +286,6 @@ __global__ void __launch_bounds__(256) sc_linear_direct_kernel(const ScArgs a) {
   }
 }
 
-// Sector 2D / pyramid 3D: one warp per output row (iz, iy), 8 rows per CTA,
-// and a group of `fpc` frames per CTA.  Lane l takes x = x0 + 32 j + l
-// (j < 4: coalesced 8-byte entry loads and output stores); each entry is
-// read ONCE and applied to every frame of the group (the table, not the
-// L2-resident line image, is the HBM traffic), so a frame costs the gathers,
-// the blend and the output store.  Offsets are 32-bit (L * S < 2^31 and the
-// table < 2^32 entries, checked at create).
 // u32 -> f32 on the full-rate ALU path (I2FP.F32.U32); the compiler's
 // choice for values it knows to be 8/16-bit, I2F.U16, runs at quarter rate.
 __device__ __forceinline__ float u2f(uint32_t x) {
@@ -302,22 +295,21 @@ __device__ __forceinline__ float u2f(uint32_t x) {
 }
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 
-// Sector 2D / pyramid 3D: one warp per output row (iz, iy), 8 rows per CTA,
-// and a group of `fpc` frames per CTA.  Lane l takes x = x0 + 32 j + l
-// (j < 4: coalesced 8-byte entry loads and output stores); each entry is
-// read ONCE and applied to every frame of the group, so a frame costs the
-// corner gathers of the L2-resident line image, the blend and the store.
+// Sector 2D / pyramid 3D: each warp walks output rows (iz, iy) with a
+// stride of the grid's warp count, for a group of `fpc` frames per CTA.
+// Over the row's valid column range [xlo, xhi) lane l takes
+// x = x0 + 32 j + l (j < 4: coalesced 8-byte entry loads and output
+// stores); the columns outside it are written as zeros.  Each entry is read
+// ONCE and applied to every frame of the group, so a frame costs the corner
+// gathers of the L2-resident line image, the blend and the store.  While a
+// row is blended the next row's record is loaded and its entry span
+// bulk-prefetched into L2 (the entry loads were the DRAM-latency stall:
+// long-scoreboard on the first use of each entry, ~18 % of samples).
 // Offsets within a frame are 32-bit (L * S < 2^31, checked at create).
-// Measured (C4, u8 line image): bound by the L1 gather path (l1tex data
-// pipe ~70 %, long-scoreboard stalls on the corner loads), not by DRAM;
-// staging each row block's entries in shared memory with bulk copies
-// (double-buffered, persistent CTAs) or z-major warp tiles (4 x by 8 z per
-// warp, ~5 L1 lines per gather instead of ~15) were both slower
-// (60 vs 52 us per C4 volume).
-// Rows are walked by each warp with a stride of the grid's warp count; the
-// next row's record is loaded and its entry span bulk-prefetched into L2
-// while the current row is blended (the entry loads were the DRAM-latency
-// stall: long-scoreboard on the first use of each entry, ~18 % of samples).
+// Measured (C4p, u8 line image): latency-bound on the corner gathers
+// (long-scoreboard 45 % of the stall samples), not by DRAM (22 %); staging
+// the entries in shared memory (bulk copies, per-warp double buffers or
+// per-CTA row blocks) and z-major warp tiles were slower.
 __device__ __forceinline__ void l2_prefetch_span(const void* p, uint32_t bytes) {
   const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
   const uint32_t n = (uint32_t)((((uintptr_t)p + bytes + 15) & ~(uintptr_t)15) - a0);
@@ -342,105 +334,105 @@ __global__ void __launch_bounds__(256, 4) sc_table_kernel(const ScArgs a, int fp
   prefetch_row(nrow);
   ScRow nnrow = r + rstride < nrows ? a.rows[r + rstride] : nrow;
   for (; r < nrows; r += rstride) {
-  const ScRow row = nrow;
-  if (r + rstride < nrows) {
-    // next row: its entries into L2 now; the record after it loads while
-    // this row is blended
-    nrow = nnrow;
-    prefetch_row(nrow);
-    if (r + 2 * rstride < nrows) nnrow = a.rows[r + 2 * rstride];
-  }
-  const uint32_t S = (uint32_t)a.S, LS = (uint32_t)a.Lx * S;
-  const size_t fstride = (size_t)a.Ly * LS;  // line-image elements per frame
-  const size_t ostride = (size_t)a.nz * a.ny * a.nx;
-  const float fy = row.fy;
-  using InT = typename std::conditional<IN_T == SUPRA_T_U8, uint8_t, float>::type;
-  // u8 line images are blended as integers 0..255 (exact in f32) and scaled
-  // by 1/255 once at the end
-  constexpr float kInScale = IN_T == SUPRA_T_U8 ? 1.0f / 255.0f : 1.0f;
-  const uint2* rent = reinterpret_cast<const uint2*>(a.ent) + row.off - row.xlo;  // entry of column x: rent[x]
-  // columns outside the row's valid range [xlo, xhi): zeros (and mask 0)
-  {
-    const int xlo = max(0, min(row.xlo, a.nx)), xhi = max(xlo, min(row.xhi, a.nx));
-    for (int f = f0; f < f1; f++) {
-      const size_t ob = (size_t)f * ostride + (size_t)r * a.nx;
-      for (int x = lane; x < xlo; x += 32) {
-        if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = 0;
-        else ((float*)a.img)[ob + x] = 0.f;
+    const ScRow row = nrow;
+    if (r + rstride < nrows) {
+      // next row: its entries into L2 now; the record after it loads while
+      // this row is blended
+      nrow = nnrow;
+      prefetch_row(nrow);
+      if (r + 2 * rstride < nrows) nnrow = a.rows[r + 2 * rstride];
+    }
+    const uint32_t S = (uint32_t)a.S, LS = (uint32_t)a.Lx * S;
+    const size_t fstride = (size_t)a.Ly * LS;  // line-image elements per frame
+    const size_t ostride = (size_t)a.nz * a.ny * a.nx;
+    const float fy = row.fy;
+    using InT = typename std::conditional<IN_T == SUPRA_T_U8, uint8_t, float>::type;
+    // u8 line images are blended as integers 0..255 (exact in f32) and scaled
+    // by 1/255 once at the end
+    constexpr float kInScale = IN_T == SUPRA_T_U8 ? 1.0f / 255.0f : 1.0f;
+    const uint2* rent = reinterpret_cast<const uint2*>(a.ent) + row.off - row.xlo;  // entry of column x: rent[x]
+    // columns outside the row's valid range [xlo, xhi): zeros (and mask 0)
+    {
+      const int xlo = max(0, min(row.xlo, a.nx)), xhi = max(xlo, min(row.xhi, a.nx));
+      for (int f = f0; f < f1; f++) {
+        const size_t ob = (size_t)f * ostride + (size_t)r * a.nx;
+        for (int x = lane; x < xlo; x += 32) {
+          if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = 0;
+          else ((float*)a.img)[ob + x] = 0.f;
+        }
+        for (int x = xhi + lane; x < a.nx; x += 32) {
+          if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = 0;
+          else ((float*)a.img)[ob + x] = 0.f;
+        }
       }
-      for (int x = xhi + lane; x < a.nx; x += 32) {
-        if constexpr (OUT_T == SUPRA_T_U8) ((uint8_t*)a.img)[ob + x] = 0;
-        else ((float*)a.img)[ob + x] = 0.f;
+      if (a.mask && f0 == 0) {
+        for (int x = lane; x < xlo; x += 32) a.mask[(size_t)r * a.nx + x] = 0;
+        for (int x = xhi + lane; x < a.nx; x += 32) a.mask[(size_t)r * a.nx + x] = 0;
       }
     }
-    if (a.mask && f0 == 0) {
-      for (int x = lane; x < xlo; x += 32) a.mask[(size_t)r * a.nx + x] = 0;
-      for (int x = xhi + lane; x < a.nx; x += 32) a.mask[(size_t)r * a.nx + x] = 0;
-    }
-  }
-  // the valid range, in chunks of 32 V columns
-  const int xend = min(row.xhi, a.nx);
-  for (int x0 = max(0, row.xlo); x0 < xend; x0 += 32 * V) {
-    uint32_t base[V];
-    float fx[V], fz[V];
-#pragma unroll
-    for (int j = 0; j < V; j++) {
-      const int x = x0 + 32 * j + lane;
-      base[j] = kScInvalid;
-      uint32_t q = 0u;
-      if (x >= row.xlo && x < row.xhi) {
-        const uint2 e = __ldg(rent + x);
-        base[j] = e.x;
-        q = e.y;
-      }
-      fx[j] = u2f(q & 0xFFFFu) * (1.0f / 65535.0f);
-      fz[j] = u2f(q >> 16) * (1.0f / 65535.0f);
-      if (a.mask && f0 == 0 && x < xend) a.mask[(size_t)r * a.nx + x] = base[j] != kScInvalid ? 1 : 0;
-    }
-    for (int f = f0; f < f1; f++) {
-      float ref = 0.f, lref = 0.f;
-      if constexpr (LOGLOAD) {
-        ref = __uint_as_float(a.frame_max[f]);
-        lref = ref > 0.f ? lg2_approx(ref) : 0.f;
-      }
-      const InT* lf = (const InT*)a.line_img + (size_t)f * fstride;
-      auto ld = [&](const InT* p) {
-        float y;
-        if constexpr (IN_T == SUPRA_T_U8) y = u2f(__ldg(p));
-        else y = __ldg(p);
-        if constexpr (LOGLOAD) y = y_of_env(y, ref, lref, a.DR_k);
-        return y;
-      };
-      const size_t ob = (size_t)f * ostride + (size_t)r * a.nx;
-#pragma unroll
+    // the valid range, in chunks of 32 V columns
+    const int xend = min(row.xhi, a.nx);
+    for (int x0 = max(0, row.xlo); x0 < xend; x0 += 32 * V) {
+      uint32_t base[V];
+      float fx[V], fz[V];
+  #pragma unroll
       for (int j = 0; j < V; j++) {
         const int x = x0 + 32 * j + lane;
-        float v = 0.f;
-        if (base[j] != kScInvalid) {
-          const InT* p0 = lf + base[j];  // corner (i0x, i0y, k0)
-          const InT* p1 = p0 + S;        // (i0x + 1, i0y, k0)
-          const float t0 = lerpf(ld(p0), ld(p0 + 1), fz[j]);
-          const float t1 = lerpf(ld(p1), ld(p1 + 1), fz[j]);
-          v = lerpf(t0, t1, fx[j]);
-          if constexpr (IS3D) {
-            const InT* p2 = p0 + LS;  // (i0x, i0y + 1, k0)
-            const InT* p3 = p2 + S;
-            const float t2 = lerpf(ld(p2), ld(p2 + 1), fz[j]);
-            const float t3 = lerpf(ld(p3), ld(p3 + 1), fz[j]);
-            v = lerpf(v, lerpf(t2, t3, fx[j]), fy);
-          }
-          v *= kInScale;
+        base[j] = kScInvalid;
+        uint32_t q = 0u;
+        if (x >= row.xlo && x < row.xhi) {
+          const uint2 e = __ldg(rent + x);
+          base[j] = e.x;
+          q = e.y;
         }
-        if (x < xend) {
-          // u8 = floor(255 v + 1/2) by the magic-number floor (FADD.RM; the
-          // F2I conversion runs at quarter rate)
-          if constexpr (OUT_T == SUPRA_T_U8)
-            ((uint8_t*)a.img)[ob + x] = (uint8_t)__float_as_uint(__fadd_rd(fmaf(255.f, v, 0.5f), 12582912.0f));
-          else ((float*)a.img)[ob + x] = v;
+        fx[j] = u2f(q & 0xFFFFu) * (1.0f / 65535.0f);
+        fz[j] = u2f(q >> 16) * (1.0f / 65535.0f);
+        if (a.mask && f0 == 0 && x < xend) a.mask[(size_t)r * a.nx + x] = base[j] != kScInvalid ? 1 : 0;
+      }
+      for (int f = f0; f < f1; f++) {
+        float ref = 0.f, lref = 0.f;
+        if constexpr (LOGLOAD) {
+          ref = __uint_as_float(a.frame_max[f]);
+          lref = ref > 0.f ? lg2_approx(ref) : 0.f;
+        }
+        const InT* lf = (const InT*)a.line_img + (size_t)f * fstride;
+        auto ld = [&](const InT* p) {
+          float y;
+          if constexpr (IN_T == SUPRA_T_U8) y = u2f(__ldg(p));
+          else y = __ldg(p);
+          if constexpr (LOGLOAD) y = y_of_env(y, ref, lref, a.DR_k);
+          return y;
+        };
+        const size_t ob = (size_t)f * ostride + (size_t)r * a.nx;
+  #pragma unroll
+        for (int j = 0; j < V; j++) {
+          const int x = x0 + 32 * j + lane;
+          float v = 0.f;
+          if (base[j] != kScInvalid) {
+            const InT* p0 = lf + base[j];  // corner (i0x, i0y, k0)
+            const InT* p1 = p0 + S;        // (i0x + 1, i0y, k0)
+            const float t0 = lerpf(ld(p0), ld(p0 + 1), fz[j]);
+            const float t1 = lerpf(ld(p1), ld(p1 + 1), fz[j]);
+            v = lerpf(t0, t1, fx[j]);
+            if constexpr (IS3D) {
+              const InT* p2 = p0 + LS;  // (i0x, i0y + 1, k0)
+              const InT* p3 = p2 + S;
+              const float t2 = lerpf(ld(p2), ld(p2 + 1), fz[j]);
+              const float t3 = lerpf(ld(p3), ld(p3 + 1), fz[j]);
+              v = lerpf(v, lerpf(t2, t3, fx[j]), fy);
+            }
+            v *= kInScale;
+          }
+          if (x < xend) {
+            // u8 = floor(255 v + 1/2) by the magic-number floor (FADD.RM; the
+            // F2I conversion runs at quarter rate)
+            if constexpr (OUT_T == SUPRA_T_U8)
+              ((uint8_t*)a.img)[ob + x] = (uint8_t)__float_as_uint(__fadd_rd(fmaf(255.f, v, 0.5f), 12582912.0f));
+            else ((float*)a.img)[ob + x] = v;
+          }
         }
       }
     }
-  }
   }  // rows
 }
 
