@@ -317,6 +317,7 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "das_ms_per_launch": das_ms, "algorithmic_bytes_per_launch": alg_bytes,
                 "das_share_of_step": das_ms / ms_per_step}
+    roofline.update(counter_extras(info, F, das_ms, args.config, achieved))
 
     # N > 1: the same stream without the gather (per-rank
     # compute rate) and with the line-domain variant (u8 line images, 0.5 MB
@@ -434,6 +435,24 @@ def ncu_entry(key: str, frames: int):
         return None
 
 
+def counter_extras(info: dict, frames: int, das_ms: float, key: str, achieved_gbs=None):
+    """SURVEY 8(d)'s per-kernel report beside the roofline: Gtaps/s, the
+    fraction of the issue ceiling (warp instructions of the same launch shape
+    from profiles/das_ncu.json over the live DAS time), the fraction of the
+    nominal 8 TB/s, and the L1 / L2 sector hit rates of the ncu capture."""
+    out = {"gtaps_per_s": info["taps_per_frame"] * frames / (das_ms / 1000.0) / 1e9}
+    if achieved_gbs is not None:
+        out["frac_of_nominal_8tbs"] = achieved_gbs / 8000.0
+    e = ncu_entry(key, frames)
+    if e:
+        if e.get("warp_inst_per_launch"):
+            out["issue_frac"] = e["warp_inst_per_launch"] / (das_ms / 1000.0) / ISSUE_PEAK_WARP_INST_S
+        for k in ("l2_hit_rate", "l1_hit_rate"):
+            if k in e:
+                out[k] = e[k]
+    return out
+
+
 def hbm_roofline(info: dict, frames: int, L: int, Sd: int, das_ms: float, key: str):
     """DAS HBM roofline: algorithmic bytes = referenced int16 input (distinct
     samples any tap reads, host-counted at create) + the f32 envelope written
@@ -442,9 +461,11 @@ def hbm_roofline(info: dict, frames: int, L: int, Sd: int, das_ms: float, key: s
     peak, kind = measured_peak_hbm()
     ach = alg / (das_ms / 1000.0) / 1e9
     e = ncu_entry(key, frames)
-    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "traffic": e.get("dram_bytes_per_launch") if e else None, "peak_kind": peak_kind_str(kind),
-            "das_ms_per_call": das_ms, "algorithmic_bytes_per_call": alg}
+    out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+           "traffic": e.get("dram_bytes_per_launch") if e else None, "peak_kind": peak_kind_str(kind),
+           "das_ms_per_call": das_ms, "algorithmic_bytes_per_call": alg}
+    out.update(counter_extras(info, frames, das_ms, key, ach))
+    return out
 
 
 def alu_roofline(info: dict, frames: int, das_ms: float, key: str):
@@ -468,6 +489,7 @@ def alu_roofline(info: dict, frames: int, das_ms: float, key: str):
                     "inst_source": "profiles/das_ncu.json (ncu --set full)"})
     else:
         out.update({"achieved": None, "frac": None})
+    out.update({k: v for k, v in counter_extras(info, frames, das_ms, key).items() if k in ("l2_hit_rate", "l1_hit_rate")})
     return out
 
 

@@ -3,10 +3,11 @@ run on the GPU box).  For every bench line it captures the DAS launches of
 ONE beamform call with
 
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
-                dram__bytes_write.sum,smsp__inst_executed.sum
+                dram__bytes_write.sum,smsp__inst_executed.sum,
+                lts__t_sector_hit_rate.pct,l1tex__t_sector_hit_rate.pct
 
 and writes profiles/das_ncu.json entries {frames, dram_bytes_per_launch,
-warp_inst_per_launch, ...} summed over the call's DAS launches (main +
+warp_inst_per_launch, l2_hit_rate, l1_hit_rate, ...} summed over the call's DAS launches (main +
 remainder).  ncu replays each kernel, so times here are cold-cache and
 serialised: only the counters are used.
 
@@ -27,7 +28,8 @@ SHAPES = {
     "T1_64_1": ("T1_64_1", 64, 1), "T1_64_2": ("T1_64_2", 64, 1),
     "T1_128_1": ("T1_128_1", 64, 1), "T1_128_2": ("T1_128_2", 64, 1),
 }
-METRICS = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum"
+METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,"
+           "lts__t_sector_hit_rate.pct,l1tex__t_sector_hit_rate.pct")
 
 
 def capture(cfg, F, nl, reps=3):
@@ -66,6 +68,11 @@ def main():
              "dram_write": sum(l["dram__bytes_write.sum"] for l in launches),
              "warp_inst_per_launch": sum(l["smsp__inst_executed.sum"] for l in launches),
              "ncu_time_ms": sum(l["gpu__time_duration.sum"] for l in launches) / 1e6}
+        # hit rates of the call's launches, weighted by their (ncu) time
+        tw = sum(l["gpu__time_duration.sum"] for l in launches)
+        for m, key in (("lts__t_sector_hit_rate.pct", "l2_hit_rate"), ("l1tex__t_sector_hit_rate.pct", "l1_hit_rate")):
+            if all(m in l for l in launches):
+                e[key] = sum(l[m] * l["gpu__time_duration.sum"] for l in launches) / tw / 100.0
         e["dram_bytes_per_launch"] = e["dram_read"] + e["dram_write"]
         db[k] = e
         print(k, json.dumps(e), flush=True)
