@@ -324,3 +324,29 @@ def test_short_first_pass(S):
     rf_o, env_o = oracle_chain(w, raw[0].cpu().numpy())
     assert rf_err(rf1[0], rf_o) <= RF_TOL
     bf.close()
+
+
+# ----------------- table scan conversion (sector 2D, pyramid 3D) from a u8
+# line image, the bench's 3D lines: the row-walking kernel blends the bytes
+# as integers and scales by 1/255 once; vs the oracle on y = v / 255.
+@pytest.mark.parametrize("name,F", [("C3", 3), ("C4b", 1)])
+def test_table_sc_u8_line_image(name, F):
+    w = configs.CONFIGS[name]().replace(line_output_type=configs.T_U8, sc_output_type=configs.T_F32)
+    g = torch.Generator().manual_seed(11)
+    li8 = torch.randint(0, 256, (F, w.L, w.S), generator=g, dtype=torch.uint8)
+    bf = SupraBF(w, max_frames=F)
+    img, mask = bf.empty_img(F), bf.empty_mask()
+    bf.scanconvert(li8.cuda(), F, img, mask)
+    wu = w.replace(sc_output_type=configs.T_U8)
+    bfu = SupraBF(wu, max_frames=F)
+    imgu = bfu.empty_img(F)
+    bfu.scanconvert(li8.cuda(), F, imgu)
+    torch.cuda.synchronize()
+    f = F - 1
+    img_o, mask_o = oracle.scan_convert(w, li8[f].numpy().astype(np.float64) / 255.0)
+    assert np.array_equal(mask.cpu().numpy().reshape(mask_o.shape), mask_o)
+    assert db_err(img.cpu().numpy()[f].reshape(img_o.shape), img_o) <= DB_TOL
+    d = imgu.cpu().numpy()[f].reshape(img_o.shape).astype(int) - oracle.to_u8(img_o).astype(int)
+    assert np.max(np.abs(d)) <= 1
+    bf.close()
+    bfu.close()
